@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: BART MCMC iterations/s on B200 (BASELINE.json metric).
+
+Workload (default, BASELINE configs[2], the metric's config): gbart on
+synthetic Friedman #1 data, n=1e6, p=100, ntree=200, D=6, 100 uniform
+cutpoints.  A "step" is one full MCMC iteration (propose + sequential sweep
+over all 200 trees + sigma draw) on resident device state.
+
+  value     iterations/s of CUDA-graph-replayed device-RNG steps, CUDA events
+            on the chain's stream, max over ranks; inputs (X 100 MB, leaf
+            index 200 MB) exceed the 126 MB L2, no flush needed.
+  e2e       the same metric through the reference-facing call
+            `step(state, hp, rng=numpy Generator)`: host StepRandoms draw,
+            H2D copy of that block, the step, and a D2H read of
+            last_accepted + sigma2 every step.
+  roofline  the sweep kernel: algorithmic bytes 10*n*m per launch (SURVEY.md
+            §8d) / mean per-launch CUDA-event duration, vs measured HBM peak.
+  cpu_baseline  the CPU oracle (numpy port of the reference, oracle/) on a
+            bounded sample: full n and p, 10 trees, scaled to 200 trees.
+
+`--impl reference` times the CPU oracle port with all host cores
+(independent chains, one per core) on the same workload and prints the same
+JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MCMC iters/sec at n=1e6,p=100,ntree=200 (1/2/4/8 B200) vs host CPU; HBM GB/s"
+CPU_SAMPLE_TREES = 10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--p", type=int, default=100)
+    ap.add_argument("--m", type=int, default=200)
+    ap.add_argument("--depth", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_2410_23244_b200.dgp import friedman1_binned
+    from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
+
+    Xq, y, _, grid = friedman1_binned(args.n, args.p, seed=args.seed)
+    hp, ys = derive_hyperparams(y, FitConfig(n_trees=args.m, max_depth=args.depth))
+    return Xq, grid.counts, ys.forward(y).astype(np.float32), hp
+
+
+def config_dict(args, parallelism):
+    return {
+        "workload": f"gbart Friedman#1 n={args.n:g} p={args.p} ntree={args.m} D={args.depth} "
+                    f"(BASELINE.json configs[2])",
+        "n": args.n, "p": args.p, "ntree": args.m, "max_depth": args.depth, "n_cutpoints": 100,
+        "parallelism": parallelism,
+        "l2": "no flush: X (n*p B) + leaf index (n*m B) per iteration exceed the 126 MB L2",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0:
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic():
+    """dram bytes per sweep launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- CPU side
+def _cpu_worker(args_tuple):
+    Xq, max_cuts, y32, hp_fields, m_sample, steps, seed = args_tuple
+    from types import SimpleNamespace
+
+    from oracle.bart_oracle import OracleChain
+
+    hp = SimpleNamespace(**hp_fields)
+    hp.n_trees = m_sample
+    ch = OracleChain(Xq, max_cuts, y32, hp)
+    rng = np.random.default_rng(seed)
+    size = 1 << hp.max_depth
+    times = []
+    for s in range(steps + 1):  # first step is warm-up
+        u = rng.random((m_sample, 5))
+        acc = rng.random(m_sample)
+        z = rng.standard_normal((m_sample, size))
+        chi2 = float(rng.chisquare(hp.nu + y32.size))
+        t0 = time.perf_counter()
+        ch.step(u, acc, z, chi2)
+        if s > 0:
+            times.append(time.perf_counter() - t0)
+    return statistics.median(times)
+
+
+def _hp_fields(hp):
+    return dict(leaf_sd=hp.leaf_sd, lam=hp.lam, n_trees=hp.n_trees, alpha=hp.alpha, beta=hp.beta,
+                leaf_mean=hp.leaf_mean, nu=hp.nu, max_depth=hp.max_depth, p_grow=hp.p_grow,
+                update_sigma=hp.update_sigma)
+
+
+def cpu_oracle_rate(Xq, max_cuts, y32, hp, m_full, steps, procs=1):
+    """Per-chain iters/s of the oracle, sampled with CPU_SAMPLE_TREES trees and scaled to m_full."""
+    job = (Xq, max_cuts, y32, _hp_fields(hp), CPU_SAMPLE_TREES, steps)
+    if procs <= 1:
+        t = _cpu_worker(job + (0,))
+        per_chain = [t]
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            per_chain = pool.map(_cpu_worker, [job + (k,) for k in range(procs)])
+    scale = m_full / CPU_SAMPLE_TREES
+    rates = [1.0 / (t * scale) for t in per_chain]
+    return sum(rates), per_chain
+
+
+# ---------------------------------------------------------------- GPU side
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def run_ours(args):
+    world, rank, local = dist_setup(args)
+    from paper_2410_23244_b200 import _build
+
+    if rank == 0:
+        _build.build()
+    barrier(world)
+    from paper_2410_23244_b200 import _native as N
+    from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run, step
+
+    Xq, max_cuts, y32, hp = workload(args)
+    # replicas: every rank runs an independent chain of the full workload
+    st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local)
+    cfg = st.sweep_config()
+    run(st, hp, args.warmup)
+    st.sync()
+    launches0 = st.kernel_launches()
+    barrier(world)
+    ms = np.zeros(1, np.float32)
+    with ClockSampler(local) as clk:
+        N.check(N.lib().bart_run_timed(st.handle, args.steps, N.ptr(ms)))
+    gpu_launches = st.kernel_launches() - launches0
+    st._after_step(args.steps)
+    barrier(world)
+    t_max = allreduce_max(float(ms[0]) / 1e3, world)
+    value = world * args.steps / t_max
+
+    # per-kernel durations (events around each launch, not graph-replayed)
+    prof = np.zeros(3, np.float32)
+    kp = max(10, min(args.steps, 50))
+    N.check(N.lib().bart_profile(st.handle, kp, N.ptr(prof)))
+    st._after_step(kp)
+    sweep_ms = float(prof[1]) / kp
+    propose_ms = float(prof[2]) / kp
+    alg_bytes = 10.0 * args.n * args.m
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
+
+    # e2e through the reference-facing call with host random blocks
+    rng = np.random.default_rng(rank)
+    m, size = args.m, 1 << args.depth
+    h2d = 8 * (5 * m + m + m * size) + 8
+    d2h = m + 8
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step(st, hp, rng=rng)
+        _ = st.last_accepted
+        _ = st.sigma2
+    e2e_s = allreduce_max(time.perf_counter() - t0, world)
+    e2e = world * args.e2e_steps / e2e_s
+    graph = bool(N.lib().bart_graph_active(st.handle))
+    st.close()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rate, per = cpu_oracle_rate(Xq, max_cuts, y32, hp, args.m, args.cpu_steps, procs=1)
+        cpu = {"value": rate, "unit": "iters/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/bart_oracle.py (numpy port of bforge.sampler.step) at n={args.n}, p={args.p} "
+                         f"with {CPU_SAMPLE_TREES} trees, median of {args.cpu_steps} steps "
+                         f"({statistics.median(per):.2f} s), scaled x{args.m // CPU_SAMPLE_TREES} to {args.m} trees"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 resid / f64 sums / u8 indices",
+            "data": "synthetic Friedman #1 (binned uint8), device Philox RNG",
+            "config": config_dict(args, "replicas" if world > 1 else "single chain, 1 GPU"),
+            "e2e": {"value": e2e, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "sampler.step(state, hp, rng=numpy Generator): host StepRandoms + H2D + step + "
+                            "D2H last_accepted/sigma2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": committed_traffic(),
+                         "kernel": "sweep_kernel", "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_ms": sweep_ms, "propose_ms": propose_ms, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "gpu_launches": gpu_launches,
+            "cuda_graph": graph,
+            "sweep_grid": cfg,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    Xq, max_cuts, y32, hp = workload(args)
+    procs = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    rates = []
+    for _ in range(max(1, args.steps if args.steps <= 3 else 1)):
+        rate, per = cpu_oracle_rate(Xq, max_cuts, y32, hp, args.m, args.cpu_steps, procs=procs)
+        rates.append(rate)
+    wall = time.perf_counter() - t0
+    value = statistics.median(rates)
+    sample = (f"oracle port (numpy restatement of bforge.sampler.step; the reference is pure Python and is not "
+              f"buildable) at n={args.n}, p={args.p}: {procs} independent chains (one per core), each "
+              f"{CPU_SAMPLE_TREES} trees x {args.cpu_steps} steps, per-tree time scaled to {args.m} trees")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value * procs,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 resid / f64 sums",
+        "data": "synthetic Friedman #1 (binned uint8)", "config": config_dict(args, f"{procs} CPU chains"),
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * bart_b200.h — C ABI of the B200-native BART MCMC step.
+ *
+ * The reference (`bforge`, /root/reference/pkg/src/bforge) is pure Python and
+ * has no FFI layer; its hot-path boundary is the Python pair
+ *     init_state(X, max_cuts, y, hp, rng, sigma2=None) -> SamplerState   (sampler.py:201-241)
+ *     step(state, hp, rng=None) -> SamplerState                           (sampler.py:878-912)
+ * plus the forest kernels traverse_forest / sum_leaf_values / evaluate_forest
+ * (trees.py:174-223).  Each entry point below names the reference function it
+ * replaces.  Plain pointers and sizes only: host arrays in the reference's own
+ * layouts ((n,p) X, (n,m) leaf index, (m,2^(D-1)) axis/cutpoint, (m,2^D) leaf
+ * values); the library owns all device memory.  A ctypes binding is in
+ * INTEGRATION.md and paper_2410_23244_b200/_native.py.
+ *
+ * Errors: every function returns BART_OK (0) or a status code; the message of
+ * the last failure on the calling thread is returned by bart_last_error().
+ * BART_EINVAL maps to the reference's ValueError (shape/config checks,
+ * sampler.py:214-217, trees.py:63-67), BART_ECUDA / BART_ESTATE to RuntimeError.
+ * Threading: one writer per handle; handles are independent.
+ */
+#ifndef BART_B200_H
+#define BART_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BART_OK 0
+#define BART_EINVAL 1
+#define BART_ECUDA 2
+#define BART_ESTATE 3
+
+#define BART_MAX_DEPTH 8 /* trees.py:27-28: leaf heap index fits one byte */
+
+typedef struct bart_chain bart_chain; /* one chain (or one n-shard of it) on one device */
+
+typedef struct {
+  int64_t n;         /* points held by this handle */
+  int32_t p;         /* predictors (axes) */
+  int32_t m;         /* trees */
+  int32_t max_depth; /* D in [1, 8] */
+  int32_t _pad;
+} bart_dims;
+
+/* sampler.Hyperparams (sampler.py:62-104).  depth_prob[d] = alpha/(1+d)**beta
+ * with depth_prob[D-1] = 0, computed by the host exactly as sampler.py:107-113. */
+typedef struct {
+  double leaf_sd, lam, alpha, beta, leaf_mean, nu, p_grow;
+  int32_t update_sigma;
+  int32_t _pad;
+  double depth_prob[BART_MAX_DEPTH];
+} bart_hparams;
+
+/* sampler.StepRandoms (sampler.py:244-260), host pointers. */
+typedef struct {
+  const double *move_u;   /* (m, 5): move coin, leaf, axis, cut, prune picks */
+  const double *accept_u; /* (m,) */
+  const double *leaf_z;   /* (m, 2^D) */
+  double chi2;
+} bart_randoms;
+
+/* Number of int64 rows written by bart_get_proposals (sampler.Proposals,
+ * sampler.py:286-306): kind, node, axis, cut, depth, n_axes, n_splits,
+ * w_small, w_prime_big, growable_big, left_child_growable, right_child_growable. */
+#define BART_PROPOSAL_ROWS 12
+
+/* ---- chain lifecycle (replaces sampler.init_state, sampler.py:201-241) ---- */
+
+/* Root-only zero forest, leaf index == 1, resid = y (sampler.py:218-241).
+ * X is (n, p) row-major uint8 grid indices; max_cuts (p,) <= 255; y (n,) f32.
+ * seed keys the on-device Philox stream used when bart_step gets no randoms. */
+int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
+                const int64_t *max_cuts, const float *y, double sigma2, uint64_t seed,
+                int device, bart_chain **out);
+int bart_destroy(bart_chain *h);
+
+/* Direct state edit + SamplerState.rebuild_structure_caches (sampler.py:157-168,
+ * tests/util.py:11-24).  axis (m, 2^(D-1)) as uint16; leaf_index (n, m) or NULL
+ * (then recomputed by traversal); resid (n,) or NULL (then y - forest in f64,
+ * cast to f32).  sigma2 < 0 keeps the current value. */
+int bart_set_state(bart_chain *h, const uint16_t *axis, const uint8_t *cutpoint,
+                   const float *leaf_value, const uint8_t *leaf_index, const float *resid,
+                   double sigma2);
+int bart_set_hparams(bart_chain *h, const bart_hparams *hp);
+int bart_set_sigma2(bart_chain *h, double sigma2);
+
+/* ---- the hot path (replaces sampler.step, sampler.py:878-912) ----
+ * randoms != NULL: use the caller's StepRandoms (parity mode, bit-compatible
+ * with the reference's Generator stream).  randoms == NULL: draw them on the
+ * device from counter-based Philox4x32-10 keyed by (seed, iteration). */
+int bart_step(bart_chain *h, const bart_randoms *randoms);
+/* Phase 1 alone (sampler.propose_moves, sampler.py:469-526): proposals for the
+ * current forest from the given (m, 5) uniforms; the state is not changed.
+ * Read them with bart_get_proposals. */
+int bart_propose(bart_chain *h, const double *move_u);
+/* n_iter device-RNG iterations, replayed from a captured CUDA graph. Async. */
+int bart_run(bart_chain *h, int64_t n_iter);
+int bart_sync(bart_chain *h);
+
+/* ---- state readback (reference layouts) ---- */
+int bart_get_forest(bart_chain *h, uint16_t *axis, uint8_t *cutpoint, float *leaf_value);
+int bart_get_leaf_index(bart_chain *h, uint8_t *out_nm); /* (n, m) */
+int bart_get_resid(bart_chain *h, float *out);
+int bart_get_sigma2(bart_chain *h, double *out);
+int bart_get_accepted(bart_chain *h, uint8_t *out); /* last_accepted (m,) */
+int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struct_log /* (m,) */);
+/* Phase taps for parity (enable with bart_set_taps before the step):
+ * counts (m, 2^D) after the grow refresh (sampler.py:894-897) and the
+ * tree-excluded sums (m, 2^D) each tree resolved with (sampler.py:828). */
+int bart_set_taps(bart_chain *h, int on);
+int bart_get_taps(bart_chain *h, int64_t *counts, double *sums);
+int64_t bart_iteration(bart_chain *h);
+
+/* ---- predictions (trees.sum_leaf_values / evaluate_forest, trees.py:206-223) ---- */
+/* sum of trees from the cached leaf index, f64 in tree order: (n,) */
+int bart_predict_cached(bart_chain *h, double *out);
+/* evaluate the chain's current forest on a new (n_new, p) matrix */
+int bart_predict_matrix(bart_chain *h, const uint8_t *X, int64_t n_new, double *out);
+
+/* ---- stateless forest kernels (trees.traverse_forest, trees.py:174-203) ---- */
+int bart_traverse(const bart_dims *dims, const uint16_t *axis, const uint8_t *cutpoint,
+                  const uint8_t *X, uint8_t *out_nm, int device);
+int bart_evaluate(const bart_dims *dims, const uint16_t *axis, const uint8_t *cutpoint,
+                  const float *leaf_value, const uint8_t *X, double *out, int device);
+/* n_forests forests stacked (F, m, ...) on one (n, p) matrix: out (F, n)
+ * (regression.predict over kept forests, regression.py:252-258). */
+int bart_evaluate_many(const bart_dims *dims, int64_t n_forests, const uint16_t *axis, const uint8_t *cutpoint,
+                       const float *leaf_value, const uint8_t *X, double *out, int device);
+/* trees.sum_leaf_values (trees.py:206-218) on host arrays: leaf (m, 2^D), L (n, m) */
+int bart_sum_leaf_values(const bart_dims *dims, const float *leaf_value, const uint8_t *leaf_index_nm,
+                         double *out, int device);
+
+/* ---- measurement hooks used by bench.py ---- */
+/* Runs n_iter device-RNG iterations with CUDA events on the chain's stream:
+ * ms[0] = total elapsed, ms[1] = summed sweep-kernel time, ms[2] = summed
+ * propose-kernel time (per-launch events, not graph-replayed). */
+int bart_profile(bart_chain *h, int64_t n_iter, float *ms);
+/* n_iter graph-replayed device-RNG iterations bracketed by CUDA events on the
+ * chain's stream (synchronised on both sides); *ms = elapsed. */
+int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms);
+/* kernels this library launched on the handle since creation */
+int64_t bart_kernel_launches(bart_chain *h);
+/* 1 if bart_run replays a captured CUDA graph, 0 if it falls back to launches */
+int bart_graph_active(bart_chain *h);
+int bart_sweep_config(bart_chain *h, int32_t *out /* [ctas, threads, chunk, smem_bytes] */);
+
+const char *bart_last_error(void);
+const char *bart_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BART_B200_H */

@@ -1,0 +1,708 @@
+// C ABI (include/bart_b200.h): chain handles, host<->device layout changes,
+// step orchestration (propose kernel + persistent sweep, optionally replayed
+// from a CUDA graph), readback taps and measurement hooks.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bart_b200.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace bart;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess) return fail(BART_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+}
+
+struct DevBuf {  // scoped temporary device buffer
+  void *p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+  template <typename T>
+  T *as() {
+    return reinterpret_cast<T *>(p);
+  }
+};
+
+int64_t round16(int64_t v) { return (v + 15) & ~int64_t(15); }
+
+int check_dims(const bart_dims *d) {
+  if (!d) return fail(BART_EINVAL, "dims is NULL");
+  if (d->max_depth < 1 || d->max_depth > BART_MAX_DEPTH)
+    return fail(BART_EINVAL, "max_depth must be in [1, 8], got " + std::to_string(d->max_depth));
+  if (d->m < 1) return fail(BART_EINVAL, "n_trees must be >= 1, got " + std::to_string(d->m));
+  if (d->n < 1) return fail(BART_EINVAL, "need at least one point");
+  if (d->p < 1 || d->p > 65536) return fail(BART_EINVAL, "p must be in [1, 65536]");
+  return BART_OK;
+}
+
+HP to_hp(const bart_hparams *h) {
+  HP o;
+  o.leaf_sd = h->leaf_sd;
+  o.lam = h->lam;
+  o.alpha = h->alpha;
+  o.beta = h->beta;
+  o.leaf_mean = h->leaf_mean;
+  o.nu = h->nu;
+  o.p_grow = h->p_grow;
+  o.update_sigma = h->update_sigma;
+  for (int i = 0; i < kMaxDepth; ++i) o.depth_prob[i] = h->depth_prob[i];
+  return o;
+}
+
+}  // namespace
+
+struct bart_chain {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ChainDev c{};
+  size_t smem = 0;
+  int64_t iteration = 0;
+  uint64_t tag_next = 0;  // host mirror of the device tag base
+  int64_t launches = 0;
+  bool taps_on = false;
+  cudaGraphExec_t graph = nullptr;
+  bool graph_failed = false;
+  std::vector<void *> owned;
+};
+
+namespace {
+
+void free_chain(bart_chain *h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (void *p : h->owned)
+    if (p) cudaFree(p);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+template <typename T>
+cudaError_t own(bart_chain *h, T **p, size_t count) {
+  cudaError_t e = dalloc(p, count);
+  if (e == cudaSuccess) {
+    h->owned.push_back(*p);
+    e = cudaMemsetAsync(*p, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16, h->stream);
+  }
+  return e;
+}
+
+int reset_mailbox_if_needed(bart_chain *h, int64_t iters) {
+  const uint64_t need = (uint64_t)(h->c.m + 1) * (uint64_t)(iters > 0 ? iters : 1);
+  if (h->tag_next + need < 0xFFFFFFF0ull) return BART_OK;
+  const size_t words = (size_t)2 * (kSlotsMax + 1) * h->c.nblk * 4;
+  CUDA_TRY(cudaMemsetAsync(h->c.mbox, 0, words * sizeof(unsigned long long), h->stream));
+  CUDA_TRY(cudaMemsetAsync(h->c.tagbase, 0, sizeof(uint32_t), h->stream));
+  h->tag_next = 0;
+  if (need >= 0xFFFFFFF0ull) return fail(BART_EINVAL, "too many iterations in one call");
+  return BART_OK;
+}
+
+int launch_iteration(bart_chain *h, int device_rng) {
+  launch_propose(h->c, device_rng, h->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
+  h->launches += 2;
+  h->tag_next += (uint64_t)(h->c.m + 1);
+  h->iteration += 1;
+  return BART_OK;
+}
+
+int ensure_graph(bart_chain *h) {
+  if (h->graph || h->graph_failed) return BART_OK;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    h->graph_failed = true;
+    cudaGetLastError();
+    return BART_OK;
+  }
+  launch_propose(h->c, 1, h->stream);
+  cudaError_t e1 = cudaGetLastError();
+  cudaError_t e2 = (cudaError_t)sweep_launch(h->c, h->smem, h->stream);
+  cudaError_t e3 = cudaStreamEndCapture(h->stream, &g);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || !g ||
+      cudaGraphInstantiate(&h->graph, g, 0) != cudaSuccess) {
+    h->graph = nullptr;
+    h->graph_failed = true;
+    cudaGetLastError();
+  }
+  if (g) cudaGraphDestroy(g);
+  return BART_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bart_last_error(void) { return g_err.c_str(); }
+const char *bart_version(void) { return "bart_b200 0.1 sm_100a"; }
+
+int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
+                const float *y, double sigma2, uint64_t seed, int device, bart_chain **out) {
+  if (int rc = check_dims(dims)) return rc;
+  if (!hp || !X || !max_cuts || !y || !out) return fail(BART_EINVAL, "NULL argument");
+  for (int a = 0; a < dims->p; ++a)
+    if (max_cuts[a] < 0 || max_cuts[a] > 255)
+      return fail(BART_EINVAL, "max_cuts must be in [0, 255] (grid.py:18)");
+  CUDA_TRY(cudaSetDevice(device));
+  bart_chain *h = new bart_chain();
+  h->device = device;
+  auto bail = [&](int rc) {
+    free_chain(h);
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(BART_ECUDA, "cudaStreamCreate failed"));
+
+  ChainDev &c = h->c;
+  c.n = dims->n;
+  c.n_pad = round16(dims->n);
+  c.p = dims->p;
+  c.m = dims->m;
+  c.D = dims->max_depth;
+  c.half = 1 << (c.D - 1);
+  c.size = 1 << c.D;
+  c.hp = to_hp(hp);
+  c.seed = seed;
+
+  // sweep geometry: one CTA per SM, contiguous 16-aligned chunks
+  int sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  int64_t want = (c.n + 1023) / 1024;
+  int nblk = (int)(want < sms ? (want > 0 ? want : 1) : sms);
+  if (nblk > kMaxCtas) nblk = kMaxCtas;
+  int64_t chunk = round16((c.n + nblk - 1) / nblk);
+  nblk = (int)((c.n + chunk - 1) / chunk);
+  c.nblk = nblk;
+  c.chunk = (int)chunk;
+  h->smem = sweep_smem_bytes(c.m, c.chunk);
+  if ((int64_t)h->smem > optin)
+    return bail(fail(BART_EINVAL, "n per device too large for the smem-resident sweep: chunk " +
+                                      std::to_string(chunk) + " points needs " + std::to_string(h->smem) +
+                                      " B shared memory > " + std::to_string(optin) + " (shard across GPUs)"));
+  if (cudaError_t e = sweep_prepare(h->smem); e != cudaSuccess)
+    return bail(fail(BART_ECUDA, std::string("sweep_prepare: ") + cudaGetErrorString(e)));
+  const int maxc = sweep_max_ctas(h->smem, device);
+  if (maxc < nblk) return bail(fail(BART_ECUDA, "sweep grid cannot be co-resident"));
+
+  const size_t np = (size_t)c.n_pad;
+  uint8_t *Xt = nullptr, *L = nullptr, *cut = nullptr, *acc = nullptr;
+  float *r = nullptr, *yy = nullptr, *leaf = nullptr;
+  uint16_t *axis = nullptr;
+  int32_t *mc = nullptr;
+  uint32_t *ob = nullptr, *tagb = nullptr;
+  TreeMove *moves = nullptr;
+  TreeHdr *hdr = nullptr;
+  double *rm = nullptr, *ra = nullptr, *rz = nullptr, *rc2 = nullptr, *s2 = nullptr, *s2d = nullptr;
+  unsigned long long *mbox = nullptr, *itd = nullptr;
+  cudaError_t e = cudaSuccess;
+#define OWN(ptr, cnt) \
+  if (e == cudaSuccess) e = own(h, &ptr, cnt)
+  OWN(Xt, (size_t)c.p * np);
+  OWN(L, (size_t)c.m * np);
+  OWN(r, np);
+  OWN(yy, np);
+  OWN(axis, (size_t)c.m * c.half);
+  OWN(cut, (size_t)c.m * c.half);
+  OWN(leaf, (size_t)c.m * c.size);
+  OWN(mc, (size_t)c.p);
+  OWN(ob, (size_t)(c.p + 31) / 32);
+  OWN(moves, (size_t)c.m);
+  OWN(hdr, (size_t)c.m);
+  OWN(rm, (size_t)c.m * 5);
+  OWN(ra, (size_t)c.m);
+  OWN(rz, (size_t)c.m * c.size);
+  OWN(rc2, 1);
+  OWN(s2, 1);
+  OWN(s2d, 1);
+  OWN(acc, (size_t)c.m);
+  OWN(mbox, (size_t)2 * (kSlotsMax + 1) * nblk * 4);
+  OWN(tagb, 1);
+  OWN(itd, 1);
+#undef OWN
+  if (e != cudaSuccess) return bail(fail(BART_ECUDA, std::string("allocation: ") + cudaGetErrorString(e)));
+  c.Xt = Xt;
+  c.L = L;
+  c.r = r;
+  c.y = yy;
+  c.axis = axis;
+  c.cut = cut;
+  c.leaf = leaf;
+  c.max_cuts = mc;
+  c.open_bits = ob;
+  c.moves = moves;
+  c.hdr = hdr;
+  c.rand_move = rm;
+  c.rand_acc = ra;
+  c.rand_z = rz;
+  c.rand_chi2 = rc2;
+  c.sigma2 = s2;
+  c.sigma2_draw = s2d;
+  c.accepted = acc;
+  c.mbox = mbox;
+  c.tagbase = tagb;
+  c.iter_dev = itd;
+
+  // predictors: (n, p) row-major -> (p, n_pad)
+  {
+    DevBuf tmp;
+    if (tmp.alloc((size_t)c.n * c.p) != cudaSuccess) return bail(fail(BART_ECUDA, "X staging alloc"));
+    if (cudaMemcpyAsync(tmp.p, X, (size_t)c.n * c.p, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+      return bail(fail(BART_ECUDA, "X upload"));
+    launch_transpose_u8(tmp.as<uint8_t>(), c.n, c.p, c.p, Xt, c.n_pad, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) return bail(fail(BART_ECUDA, "X transpose"));
+  }
+  std::vector<int32_t> mc32(c.p);
+  std::vector<uint32_t> bits((c.p + 31) / 32, 0u);
+  int popen = 0;
+  for (int a = 0; a < c.p; ++a) {
+    mc32[a] = (int32_t)max_cuts[a];
+    if (max_cuts[a] > 0) {
+      bits[a >> 5] |= 1u << (a & 31);
+      ++popen;
+    }
+  }
+  c.P_open = popen;
+  bool ok = cudaMemcpyAsync(mc, mc32.data(), mc32.size() * 4, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+            cudaMemcpyAsync(ob, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+            cudaMemcpyAsync(yy, y, (size_t)c.n * 4, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+            cudaMemcpyAsync(r, y, (size_t)c.n * 4, cudaMemcpyHostToDevice, h->stream) == cudaSuccess &&
+            cudaMemcpyAsync(s2, &sigma2, 8, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
+  if (!ok) return bail(fail(BART_ECUDA, "state upload"));
+  launch_fill_root(L, c.m, c.n, c.n_pad, h->stream);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return bail(fail(BART_ECUDA, "init kernels failed"));
+  *out = h;
+  return BART_OK;
+}
+
+int bart_destroy(bart_chain *h) {
+  free_chain(h);
+  return BART_OK;
+}
+
+int bart_set_hparams(bart_chain *h, const bart_hparams *hp) {
+  if (!h || !hp) return fail(BART_EINVAL, "NULL argument");
+  h->c.hp = to_hp(hp);
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return BART_OK;
+}
+
+int bart_set_sigma2(bart_chain *h, double sigma2) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaMemcpyAsync(h->c.sigma2, &sigma2, 8, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return BART_OK;
+}
+
+int bart_set_state(bart_chain *h, const uint16_t *axis, const uint8_t *cutpoint, const float *leaf_value,
+                   const uint8_t *leaf_index, const float *resid, double sigma2) {
+  if (!h || !axis || !cutpoint || !leaf_value) return fail(BART_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  cudaStream_t s = h->stream;
+  CUDA_TRY(cudaMemcpyAsync(c.axis, axis, (size_t)c.m * c.half * 2, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(c.cut, cutpoint, (size_t)c.m * c.half, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(c.leaf, leaf_value, (size_t)c.m * c.size * 4, cudaMemcpyHostToDevice, s));
+  if (leaf_index) {
+    DevBuf tmp;
+    CUDA_TRY(tmp.alloc((size_t)c.n * c.m));
+    CUDA_TRY(cudaMemcpyAsync(tmp.p, leaf_index, (size_t)c.n * c.m, cudaMemcpyHostToDevice, s));
+    launch_transpose_u8(tmp.as<uint8_t>(), c.n, c.m, c.m, c.L, c.n_pad, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    launch_traverse(c.Xt, c.n, c.n_pad, c.D, c.half, c.m, c.axis, c.cut, c.L, s);
+  }
+  h->launches += 1;
+  if (resid) {
+    CUDA_TRY(cudaMemcpyAsync(c.r, resid, (size_t)c.n * 4, cudaMemcpyHostToDevice, s));
+  } else {
+    DevBuf pred;
+    CUDA_TRY(pred.alloc((size_t)c.n_pad * 8));
+    launch_predict_cached(c.L, c.n, c.n_pad, c.m, c.size, c.leaf, pred.as<double>(), s);
+    launch_resid(c.y, pred.as<double>(), c.r, c.n, s);
+    h->launches += 2;
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (sigma2 >= 0.0) CUDA_TRY(cudaMemcpyAsync(c.sigma2, &sigma2, 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  return BART_OK;
+}
+
+int bart_step(bart_chain *h, const bart_randoms *rnd) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
+  if (rnd) {
+    if (!rnd->move_u || !rnd->accept_u || !rnd->leaf_z) return fail(BART_EINVAL, "incomplete randoms");
+    CUDA_TRY(cudaMemcpyAsync(c.rand_move, rnd->move_u, (size_t)c.m * 5 * 8, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(c.rand_acc, rnd->accept_u, (size_t)c.m * 8, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(c.rand_z, rnd->leaf_z, (size_t)c.m * c.size * 8, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(c.rand_chi2, &rnd->chi2, 8, cudaMemcpyHostToDevice, h->stream));
+    if (int rc = launch_iteration(h, 0)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  } else {
+    if (int rc = launch_iteration(h, 1)) return rc;
+  }
+  return BART_OK;
+}
+
+int bart_propose(bart_chain *h, const double *move_u) {
+  if (!h || !move_u) return fail(BART_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaMemcpyAsync(h->c.rand_move, move_u, (size_t)h->c.m * 5 * 8, cudaMemcpyHostToDevice, h->stream));
+  launch_propose(h->c, 0, h->stream);
+  h->launches += 1;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaGetLastError());
+  return BART_OK;
+}
+
+int bart_run(bart_chain *h, int64_t n_iter) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
+  ensure_graph(h);
+  for (int64_t i = 0; i < n_iter; ++i) {
+    if (h->graph) {
+      CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
+      h->launches += 2;
+      h->tag_next += (uint64_t)(h->c.m + 1);
+      h->iteration += 1;
+    } else if (int rc = launch_iteration(h, 1)) {
+      return rc;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  return BART_OK;
+}
+
+int bart_sync(bart_chain *h) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaGetLastError());
+  return BART_OK;
+}
+
+int bart_get_forest(bart_chain *h, uint16_t *axis, uint8_t *cutpoint, float *leaf_value) {
+  if (int rc = bart_sync(h)) return rc;
+  ChainDev &c = h->c;
+  if (axis) CUDA_TRY(cudaMemcpy(axis, c.axis, (size_t)c.m * c.half * 2, cudaMemcpyDeviceToHost));
+  if (cutpoint) CUDA_TRY(cudaMemcpy(cutpoint, c.cut, (size_t)c.m * c.half, cudaMemcpyDeviceToHost));
+  if (leaf_value) CUDA_TRY(cudaMemcpy(leaf_value, c.leaf, (size_t)c.m * c.size * 4, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_leaf_index(bart_chain *h, uint8_t *out) {
+  if (int rc = bart_sync(h)) return rc;
+  ChainDev &c = h->c;
+  DevBuf tmp;
+  CUDA_TRY(tmp.alloc((size_t)c.n * c.m));
+  launch_transpose_u8(c.L, c.m, c.n, c.n_pad, tmp.as<uint8_t>(), c.m, h->stream);
+  h->launches += 1;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaMemcpy(out, tmp.p, (size_t)c.n * c.m, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_resid(bart_chain *h, float *out) {
+  if (int rc = bart_sync(h)) return rc;
+  CUDA_TRY(cudaMemcpy(out, h->c.r, (size_t)h->c.n * 4, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_sigma2(bart_chain *h, double *out) {
+  if (int rc = bart_sync(h)) return rc;
+  CUDA_TRY(cudaMemcpy(out, h->c.sigma2, 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_accepted(bart_chain *h, uint8_t *out) {
+  if (int rc = bart_sync(h)) return rc;
+  CUDA_TRY(cudaMemcpy(out, h->c.accepted, (size_t)h->c.m, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_proposals(bart_chain *h, int64_t *rows, double *struct_log) {
+  if (int rc = bart_sync(h)) return rc;
+  const int m = h->c.m;
+  std::vector<TreeMove> mv(m);
+  CUDA_TRY(cudaMemcpy(mv.data(), h->c.moves, sizeof(TreeMove) * m, cudaMemcpyDeviceToHost));
+  for (int j = 0; j < m; ++j) {
+    const TreeMove &t = mv[j];
+    const int64_t vals[BART_PROPOSAL_ROWS] = {t.kind,    t.node,        t.axis,         t.cut,
+                                              t.depth,   t.n_axes,      t.n_splits,     t.w_small,
+                                              t.w_prime_big, t.growable_big, t.gl, t.gr};
+    for (int k = 0; k < BART_PROPOSAL_ROWS; ++k) rows[(size_t)k * m + j] = vals[k];
+    if (struct_log) struct_log[j] = t.struct_log;
+  }
+  return BART_OK;
+}
+
+int bart_set_taps(bart_chain *h, int on) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  if (on && !c.tap_counts) {
+    CUDA_TRY(own(h, &c.tap_counts, (size_t)c.m * c.size));
+    CUDA_TRY(own(h, &c.tap_sums, (size_t)c.m * c.size));
+  }
+  c.taps = on ? 1 : 0;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return BART_OK;
+}
+
+int bart_get_taps(bart_chain *h, int64_t *counts, double *sums) {
+  if (int rc = bart_sync(h)) return rc;
+  ChainDev &c = h->c;
+  if (!c.tap_counts) return fail(BART_ESTATE, "taps not enabled (bart_set_taps)");
+  CUDA_TRY(cudaMemcpy(counts, c.tap_counts, (size_t)c.m * c.size * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(sums, c.tap_sums, (size_t)c.m * c.size * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int64_t bart_iteration(bart_chain *h) { return h ? h->iteration : -1; }
+int64_t bart_kernel_launches(bart_chain *h) { return h ? h->launches : -1; }
+
+int bart_sweep_config(bart_chain *h, int32_t *out) {
+  if (!h || !out) return fail(BART_EINVAL, "NULL argument");
+  out[0] = h->c.nblk;
+  out[1] = kSweepThreads;
+  out[2] = h->c.chunk;
+  out[3] = (int32_t)h->smem;
+  return BART_OK;
+}
+
+int bart_predict_cached(bart_chain *h, double *out) {
+  if (int rc = bart_sync(h)) return rc;
+  ChainDev &c = h->c;
+  DevBuf pred;
+  CUDA_TRY(pred.alloc((size_t)c.n_pad * 8));
+  launch_predict_cached(c.L, c.n, c.n_pad, c.m, c.size, c.leaf, pred.as<double>(), h->stream);
+  h->launches += 1;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, pred.p, (size_t)c.n * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+static int evaluate_on(int device, cudaStream_t s, const ChainDev &c, const uint16_t *d_axis, const uint8_t *d_cut,
+                       const float *d_leaf, const uint8_t *X, int64_t n_new, double *out, int64_t *launches) {
+  const int64_t ld = round16(n_new);
+  DevBuf xs, xt, pred;
+  CUDA_TRY(xs.alloc((size_t)n_new * c.p));
+  CUDA_TRY(xt.alloc((size_t)ld * c.p));
+  CUDA_TRY(pred.alloc((size_t)n_new * 8));
+  CUDA_TRY(cudaMemsetAsync(xt.p, 0, (size_t)ld * c.p, s));
+  CUDA_TRY(cudaMemcpyAsync(xs.p, X, (size_t)n_new * c.p, cudaMemcpyHostToDevice, s));
+  launch_transpose_u8(xs.as<uint8_t>(), n_new, c.p, c.p, xt.as<uint8_t>(), ld, s);
+  launch_evaluate(xt.as<uint8_t>(), n_new, ld, c.D, c.half, c.m, d_axis, d_cut, d_leaf, pred.as<double>(), s);
+  if (launches) *launches += 2;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, pred.p, (size_t)n_new * 8, cudaMemcpyDeviceToHost));
+  (void)device;
+  return BART_OK;
+}
+
+int bart_predict_matrix(bart_chain *h, const uint8_t *X, int64_t n_new, double *out) {
+  if (int rc = bart_sync(h)) return rc;
+  if (n_new <= 0) return BART_OK;
+  return evaluate_on(h->device, h->stream, h->c, h->c.axis, h->c.cut, h->c.leaf, X, n_new, out, &h->launches);
+}
+
+int bart_traverse(const bart_dims *dims, const uint16_t *axis, const uint8_t *cutpoint, const uint8_t *X,
+                  uint8_t *out_nm, int device) {
+  if (int rc = check_dims(dims)) return rc;
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t n = dims->n, ld = round16(n);
+  const int m = dims->m, D = dims->max_depth, half = 1 << (D - 1), p = dims->p;
+  DevBuf da, dc, xs, xt, L, Lt;
+  CUDA_TRY(da.alloc((size_t)m * half * 2));
+  CUDA_TRY(dc.alloc((size_t)m * half));
+  CUDA_TRY(xs.alloc((size_t)n * p));
+  CUDA_TRY(xt.alloc((size_t)ld * p));
+  CUDA_TRY(L.alloc((size_t)ld * m));
+  CUDA_TRY(Lt.alloc((size_t)n * m));
+  CUDA_TRY(cudaMemset(xt.p, 0, (size_t)ld * p));
+  CUDA_TRY(cudaMemcpy(da.p, axis, (size_t)m * half * 2, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dc.p, cutpoint, (size_t)m * half, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(xs.p, X, (size_t)n * p, cudaMemcpyHostToDevice));
+  launch_transpose_u8(xs.as<uint8_t>(), n, p, p, xt.as<uint8_t>(), ld, 0);
+  launch_traverse(xt.as<uint8_t>(), n, ld, D, half, m, da.as<uint16_t>(), dc.as<uint8_t>(), L.as<uint8_t>(), 0);
+  launch_transpose_u8(L.as<uint8_t>(), m, n, ld, Lt.as<uint8_t>(), m, 0);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out_nm, Lt.p, (size_t)n * m, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_evaluate(const bart_dims *dims, const uint16_t *axis, const uint8_t *cutpoint, const float *leaf_value,
+                  const uint8_t *X, double *out, int device) {
+  if (int rc = check_dims(dims)) return rc;
+  CUDA_TRY(cudaSetDevice(device));
+  ChainDev c{};
+  c.p = dims->p;
+  c.m = dims->m;
+  c.D = dims->max_depth;
+  c.half = 1 << (c.D - 1);
+  c.size = 1 << c.D;
+  DevBuf da, dc, dl;
+  CUDA_TRY(da.alloc((size_t)c.m * c.half * 2));
+  CUDA_TRY(dc.alloc((size_t)c.m * c.half));
+  CUDA_TRY(dl.alloc((size_t)c.m * c.size * 4));
+  CUDA_TRY(cudaMemcpy(da.p, axis, (size_t)c.m * c.half * 2, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dc.p, cutpoint, (size_t)c.m * c.half, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dl.p, leaf_value, (size_t)c.m * c.size * 4, cudaMemcpyHostToDevice));
+  return evaluate_on(device, 0, c, da.as<uint16_t>(), dc.as<uint8_t>(), dl.as<float>(), X, dims->n, out, nullptr);
+}
+
+int bart_evaluate_many(const bart_dims *dims, int64_t n_forests, const uint16_t *axis, const uint8_t *cutpoint,
+                       const float *leaf_value, const uint8_t *X, double *out, int device) {
+  if (int rc = check_dims(dims)) return rc;
+  if (n_forests < 0) return fail(BART_EINVAL, "n_forests < 0");
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t n = dims->n, ld = round16(n);
+  const int m = dims->m, D = dims->max_depth, half = 1 << (D - 1), size = 1 << D, p = dims->p;
+  DevBuf xs, xt, da, dc, dl, pred;
+  CUDA_TRY(xs.alloc((size_t)n * p));
+  CUDA_TRY(xt.alloc((size_t)ld * p));
+  CUDA_TRY(da.alloc((size_t)m * half * 2));
+  CUDA_TRY(dc.alloc((size_t)m * half));
+  CUDA_TRY(dl.alloc((size_t)m * size * 4));
+  CUDA_TRY(pred.alloc((size_t)n * 8));
+  CUDA_TRY(cudaMemset(xt.p, 0, (size_t)ld * p));
+  CUDA_TRY(cudaMemcpy(xs.p, X, (size_t)n * p, cudaMemcpyHostToDevice));
+  launch_transpose_u8(xs.as<uint8_t>(), n, p, p, xt.as<uint8_t>(), ld, 0);
+  for (int64_t f = 0; f < n_forests; ++f) {
+    CUDA_TRY(cudaMemcpy(da.p, axis + (size_t)f * m * half, (size_t)m * half * 2, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dc.p, cutpoint + (size_t)f * m * half, (size_t)m * half, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dl.p, leaf_value + (size_t)f * m * size, (size_t)m * size * 4, cudaMemcpyHostToDevice));
+    launch_evaluate(xt.as<uint8_t>(), n, ld, D, half, m, da.as<uint16_t>(), dc.as<uint8_t>(), dl.as<float>(),
+                    pred.as<double>(), 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out + (size_t)f * n, pred.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  }
+  return BART_OK;
+}
+
+int bart_sum_leaf_values(const bart_dims *dims, const float *leaf_value, const uint8_t *leaf_index_nm, double *out,
+                         int device) {
+  if (int rc = check_dims(dims)) return rc;
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t n = dims->n, ld = round16(n);
+  const int m = dims->m, size = 1 << dims->max_depth;
+  DevBuf ls, L, dl, pred;
+  CUDA_TRY(ls.alloc((size_t)n * m));
+  CUDA_TRY(L.alloc((size_t)ld * m));
+  CUDA_TRY(dl.alloc((size_t)m * size * 4));
+  CUDA_TRY(pred.alloc((size_t)ld * 8));
+  CUDA_TRY(cudaMemset(L.p, 0, (size_t)ld * m));
+  CUDA_TRY(cudaMemcpy(ls.p, leaf_index_nm, (size_t)n * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dl.p, leaf_value, (size_t)m * size * 4, cudaMemcpyHostToDevice));
+  launch_transpose_u8(ls.as<uint8_t>(), n, m, m, L.as<uint8_t>(), ld, 0);
+  launch_predict_cached(L.as<uint8_t>(), n, ld, m, size, dl.as<float>(), pred.as<double>(), 0);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, pred.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
+  if (!h || !ms) return fail(BART_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
+  ensure_graph(h);
+  cudaEvent_t a, b;
+  CUDA_TRY(cudaEventCreate(&a));
+  CUDA_TRY(cudaEventCreate(&b));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaEventRecord(a, h->stream));
+  for (int64_t i = 0; i < n_iter; ++i) {
+    if (h->graph) {
+      CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
+      h->launches += 2;
+      h->tag_next += (uint64_t)(h->c.m + 1);
+      h->iteration += 1;
+    } else if (int rc = launch_iteration(h, 1)) {
+      return rc;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(b, h->stream));
+  CUDA_TRY(cudaEventSynchronize(b));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventElapsedTime(ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return BART_OK;
+}
+
+int bart_graph_active(bart_chain *h) { return h && h->graph ? 1 : 0; }
+
+int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
+  if (!h || !ms) return fail(BART_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
+  std::vector<cudaEvent_t> ev((size_t)(3 * n_iter + 2));
+  for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaEventRecord(ev[0], h->stream));
+  for (int64_t i = 0; i < n_iter; ++i) {
+    CUDA_TRY(cudaEventRecord(ev[1 + 3 * i], h->stream));
+    launch_propose(h->c, 1, h->stream);
+    CUDA_TRY(cudaEventRecord(ev[2 + 3 * i], h->stream));
+    CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
+    CUDA_TRY(cudaEventRecord(ev[3 + 3 * i], h->stream));
+    h->launches += 2;
+    h->tag_next += (uint64_t)(h->c.m + 1);
+    h->iteration += 1;
+  }
+  CUDA_TRY(cudaEventRecord(ev.back(), h->stream));
+  CUDA_TRY(cudaEventSynchronize(ev.back()));
+  float tot = 0.f, sw = 0.f, pr = 0.f, x = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&tot, ev[0], ev.back()));
+  for (int64_t i = 0; i < n_iter; ++i) {
+    CUDA_TRY(cudaEventElapsedTime(&x, ev[1 + 3 * i], ev[2 + 3 * i]));
+    pr += x;
+    CUDA_TRY(cudaEventElapsedTime(&x, ev[2 + 3 * i], ev[3 + 3 * i]));
+    sw += x;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  ms[0] = tot;
+  ms[1] = sw;
+  ms[2] = pr;
+  return BART_OK;
+}
+
+}  // extern "C"
