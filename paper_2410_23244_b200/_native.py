@@ -64,6 +64,9 @@ _SIGS = {
     "bart_profile": [_P, C.c_int64, _P],
     "bart_sweep_config": [_P, _P],
     "bart_run_timed": [_P, C.c_int64, _P],
+    "bart_set_timeline": [_P, C.c_int],
+    "bart_get_timeline": [_P, _P],
+    "bart_get_trace": [_P, _P],
     "bart_graph_active": [_P],
 }
 _I64 = {"bart_iteration": [_P], "bart_kernel_launches": [_P]}

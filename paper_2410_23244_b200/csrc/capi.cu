@@ -81,6 +81,8 @@ struct bart_chain {
   uint64_t tag_next = 0;  // host mirror of the device tag base
   int64_t launches = 0;
   bool taps_on = false;
+  long long *timeline_buf = nullptr;
+  long long *trace_buf = nullptr;
   cudaGraphExec_t graph = nullptr;
   bool graph_failed = false;
   std::vector<void *> owned;
@@ -108,14 +110,8 @@ cudaError_t own(bart_chain *h, T **p, size_t count) {
   return e;
 }
 
-int reset_mailbox_if_needed(bart_chain *h, int64_t iters) {
-  const uint64_t need = (uint64_t)(h->c.m + 1) * (uint64_t)(iters > 0 ? iters : 1);
-  if (h->tag_next + need < 0xFFFFFFF0ull) return BART_OK;
-  const size_t words = (size_t)2 * (kSlotsMax + 1) * h->c.nblk * 4;
-  CUDA_TRY(cudaMemsetAsync(h->c.mbox, 0, words * sizeof(unsigned long long), h->stream));
-  CUDA_TRY(cudaMemsetAsync(h->c.tagbase, 0, sizeof(uint32_t), h->stream));
-  h->tag_next = 0;
-  if (need >= 0xFFFFFFF0ull) return fail(BART_EINVAL, "too many iterations in one call");
+int reset_mailbox_if_needed(bart_chain *, int64_t) {
+  // the exchange accumulators and counter are monotonic and wrap safely mod 2^64
   return BART_OK;
 }
 
@@ -198,13 +194,13 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.nblk = nblk;
   c.chunk = (int)chunk;
   h->smem = sweep_smem_bytes(c.m, c.chunk);
-  if ((int64_t)h->smem > optin)
+  if (sweep_words_per_thread(c.chunk) < 0 || (int64_t)h->smem > optin)
     return bail(fail(BART_EINVAL, "n per device too large for the smem-resident sweep: chunk " +
                                       std::to_string(chunk) + " points needs " + std::to_string(h->smem) +
                                       " B shared memory > " + std::to_string(optin) + " (shard across GPUs)"));
   if (cudaError_t e = sweep_prepare(h->smem); e != cudaSuccess)
     return bail(fail(BART_ECUDA, std::string("sweep_prepare: ") + cudaGetErrorString(e)));
-  const int maxc = sweep_max_ctas(h->smem, device);
+  const int maxc = sweep_max_ctas(h->smem, device, c.chunk);
   if (maxc < nblk) return bail(fail(BART_ECUDA, "sweep grid cannot be co-resident"));
 
   const size_t np = (size_t)c.n_pad;
@@ -212,11 +208,11 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   float *r = nullptr, *yy = nullptr, *leaf = nullptr;
   uint16_t *axis = nullptr;
   int32_t *mc = nullptr;
-  uint32_t *ob = nullptr, *tagb = nullptr;
+  uint32_t *ob = nullptr;
   TreeMove *moves = nullptr;
   TreeHdr *hdr = nullptr;
   double *rm = nullptr, *ra = nullptr, *rz = nullptr, *rc2 = nullptr, *s2 = nullptr, *s2d = nullptr;
-  unsigned long long *mbox = nullptr, *itd = nullptr;
+  unsigned long long *accum = nullptr, *itd = nullptr, *ctr = nullptr, *abase = nullptr;
   cudaError_t e = cudaSuccess;
 #define OWN(ptr, cnt) \
   if (e == cudaSuccess) e = own(h, &ptr, cnt)
@@ -238,8 +234,9 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   OWN(s2, 1);
   OWN(s2d, 1);
   OWN(acc, (size_t)c.m);
-  OWN(mbox, (size_t)2 * (kSlotsMax + 1) * nblk * 4);
-  OWN(tagb, 1);
+  OWN(accum, (size_t)(kSlotsMax + 1) * kAccWords);
+  OWN(abase, (size_t)(kSlotsMax + 1) * 5 + 16);
+  OWN(ctr, 16);  // counter alone on its 128-B line
   OWN(itd, 1);
 #undef OWN
   if (e != cudaSuccess) return bail(fail(BART_ECUDA, std::string("allocation: ") + cudaGetErrorString(e)));
@@ -261,8 +258,9 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.sigma2 = s2;
   c.sigma2_draw = s2d;
   c.accepted = acc;
-  c.mbox = mbox;
-  c.tagbase = tagb;
+  c.accum = accum;
+  c.accum_base = abase;
+  c.counter = ctr;
   c.iter_dev = itd;
 
   // predictors: (n, p) row-major -> (p, n_pad)
@@ -481,6 +479,35 @@ int bart_set_taps(bart_chain *h, int on) {
     cudaGraphExecDestroy(h->graph);
     h->graph = nullptr;
   }
+  return BART_OK;
+}
+
+int bart_set_timeline(bart_chain *h, int on) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  if (on && !h->timeline_buf) CUDA_TRY(own(h, &h->timeline_buf, (size_t)3 * (c.m + 1) * 8));
+  if (on && !h->trace_buf) CUDA_TRY(own(h, &h->trace_buf, (size_t)(c.m + 1) * c.nblk * 2));
+  c.timeline = on ? h->timeline_buf : nullptr;
+  c.trace = on ? h->trace_buf : nullptr;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return BART_OK;
+}
+
+int bart_get_timeline(bart_chain *h, int64_t *out) {
+  if (int rc = bart_sync(h)) return rc;
+  if (!h->timeline_buf) return fail(BART_ESTATE, "timeline not enabled (bart_set_timeline)");
+  CUDA_TRY(cudaMemcpy(out, h->timeline_buf, (size_t)3 * (h->c.m + 1) * 8 * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_trace(bart_chain *h, int64_t *out) {
+  if (int rc = bart_sync(h)) return rc;
+  if (!h->trace_buf) return fail(BART_ESTATE, "timeline not enabled (bart_set_timeline)");
+  CUDA_TRY(cudaMemcpy(out, h->trace_buf, (size_t)(h->c.m + 1) * h->c.nblk * 2 * 8, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 

@@ -18,11 +18,14 @@ namespace bart {
 
 constexpr int kMaxDepth = 8;
 constexpr int kSlotsMax = 128;        // leaves of a depth-8 tree
-constexpr int kSweepThreads = 512;
+constexpr int kWorkers = 480;                 // threads that own points (15 warps)
+constexpr int kWorkWarps = kWorkers / 32;
+constexpr int kSweepThreads = kWorkers + 32;  // + one producer warp (TMA / stage loads)
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kMaxCtas = 256;         // mailbox gather unroll bound
 constexpr int kGatherUnroll = kMaxCtas / 32;
 constexpr int kProposeWarps = 4;
+constexpr int kAccWords = 8;       // per slot: 4 fixed-point limbs, 1 count, pad (64 B)
 
 enum : int { KIND_NONE = 0, KIND_GROW = 1, KIND_PRUNE = 2 };
 
@@ -40,13 +43,15 @@ struct __align__(16) TreeMove {
   int32_t w_prime_big, growable_big, gl, gr;
   int32_t nslots, pad0;
   double struct_log;
+  double log_u;  // log(accept_u): lets the sweep decide without exp() off the near-tie band
   uint8_t slot_node[kSlotsMax];
 };
 
 // Compact per-tree header the sweep keeps in shared memory for all trees.
 struct __align__(8) TreeHdr {
-  uint8_t kind, node, cut, pad;
-  uint16_t axis, nslots;
+  uint8_t kind, node, cut, nslots;  // nslots in [1, 128]
+  uint16_t axis;
+  uint8_t slot_l, slot_r;  // slot indices of children 2t, 2t+1 in the larger tree (moves only)
 };
 
 // Everything a kernel needs about one chain (passed by value).
@@ -71,11 +76,14 @@ struct ChainDev {
   int64_t *tap_counts;
   double *tap_sums;
   int taps;
-  unsigned long long *mbox;   // [2][kSlotsMax+1][nblk][4] LL mailbox
-  uint32_t *tagbase;
+  unsigned long long *accum;    // [kSlotsMax+1][kAccWords] monotonic fixed-point slot accumulators
+  unsigned long long *counter;  // monotonic exchange arrival counter (own 128-B line)
+  unsigned long long *accum_base;  // accumulator + counter values at the end of the last sweep
   unsigned long long *iter_dev;
   uint64_t seed;
   int nblk, chunk;
+  long long *timeline;        // optional per-tree phase stamps (clock64), CTA 0 and last CTA
+  long long *trace;           // optional (m+1, nblk, 2) globaltimer: publish, gathered
   HP hp;
 };
 
@@ -94,22 +102,6 @@ __device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
 // 53-bit uniform in [0, 1)
 __device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
   return (double)((((uint64_t)(a >> 5)) << 26) | (uint64_t)(b >> 6)) * 0x1.0p-53;
-}
-
-// ------------------------------------------------------------ LL mailbox
-// Low-latency exchange: every 64-bit word carries a 32-bit tag in its high
-// half, so a reader validates data and arrival with one load (no fences).
-__device__ __forceinline__ void ll_store(unsigned long long *p, uint32_t tag, uint32_t cnt, double s) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(s);
-  const unsigned long long t = ((unsigned long long)tag) << 32;
-  const unsigned long long w0 = t | cnt, w1 = t | (bits & 0xffffffffull), w2 = t | (bits >> 32);
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p + 2), "l"(w2) : "memory");
-}
-__device__ __forceinline__ void ll_load(const unsigned long long *p, unsigned long long &w0,
-                                        unsigned long long &w1, unsigned long long &w2) {
-  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(w2) : "l"(p + 2) : "memory");
 }
 
 // ------------------------------------------------------------ misc

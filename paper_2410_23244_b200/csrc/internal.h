@@ -12,7 +12,8 @@ namespace bart {
 void launch_propose(const ChainDev &c, int device_rng, cudaStream_t s);
 size_t sweep_smem_bytes(int m, int chunk);
 cudaError_t sweep_prepare(size_t smem);
-int sweep_max_ctas(size_t smem, int device);
+int sweep_max_ctas(size_t smem, int device, int chunk);
+int sweep_words_per_thread(int chunk);
 int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s);
 
 void launch_transpose_u8(const uint8_t *src, int64_t rows, int64_t cols, int64_t src_ld, uint8_t *dst,

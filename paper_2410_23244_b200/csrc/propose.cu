@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
   __syncwarp();
 
   // ---- the tree's random numbers (sampler.py:253-260 block layout)
-  double u[5];
+  double u[5], acc_u;
   if (device_rng) {
     double ra = 0.0, rb = 0.0;
     if (lane < 3) {
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
     u[2] = __shfl_sync(0xffffffffu, ra, 1);
     u[3] = __shfl_sync(0xffffffffu, rb, 1);
     u[4] = __shfl_sync(0xffffffffu, ra, 2);
-    const double acc_u = __shfl_sync(0xffffffffu, rb, 2);
+    acc_u = __shfl_sync(0xffffffffu, rb, 2);
     if (lane < 5) c.rand_move[(size_t)j * 5 + lane] = u[lane];
     if (lane == 0) c.rand_acc[j] = acc_u;
     for (int q = lane; 2 * q < size; q += 32) {  // Box-Muller pairs
@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
   } else {
 #pragma unroll
     for (int k = 0; k < 5; ++k) u[k] = c.rand_move[(size_t)j * 5 + k];
+    acc_u = c.rand_acc[j];
   }
 
   // ---- candidate sets in heap order (sampler.py:342-360)
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
 
   // ---- leaves of the larger tree, heap order: the sweep's histogram slots
   TreeMove &mv = c.moves[j];
-  int nslots = 0;
+  int nslots = 0, slot_l = 0, slot_r = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (k < npl) {
@@ -292,10 +293,15 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
       if (grow && h == t) big = false;
       if (grow && (h == 2 * t || h == 2 * t + 1)) big = true;
       const uint32_t b = __ballot_sync(0xffffffffu, big);
-      if (big) mv.slot_node[nslots + __popc(b & ((1u << lane) - 1u))] = (uint8_t)h;
+      const int idx = nslots + __popc(b & ((1u << lane) - 1u));
+      if (big) mv.slot_node[idx] = (uint8_t)h;
+      if (big && kind != KIND_NONE && h == 2 * t) slot_l = idx;
+      if (big && kind != KIND_NONE && h == 2 * t + 1) slot_r = idx;
       nslots += __popc(b);
     }
   }
+  slot_l = __reduce_max_sync(0xffffffffu, (unsigned)slot_l);
+  slot_r = __reduce_max_sync(0xffffffffu, (unsigned)slot_r);
   if (lane == 0) {
     mv.kind = kind;
     mv.node = t;
@@ -311,13 +317,15 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
     mv.gr = gr;
     mv.nslots = nslots;
     mv.struct_log = struct_log;
+    mv.log_u = log(acc_u);
     TreeHdr hd;
     hd.kind = (uint8_t)kind;
     hd.node = (uint8_t)t;
     hd.cut = (uint8_t)c_sel;
-    hd.pad = 0;
+    hd.nslots = (uint8_t)nslots;
     hd.axis = (uint16_t)a_sel;
-    hd.nslots = (uint16_t)nslots;
+    hd.slot_l = (uint8_t)slot_l;
+    hd.slot_r = (uint8_t)slot_r;
     c.hdr[j] = hd;
   }
 }
