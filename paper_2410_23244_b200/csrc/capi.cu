@@ -78,7 +78,6 @@ struct bart_chain {
   ChainDev c{};
   size_t smem = 0;
   int64_t iteration = 0;
-  uint64_t tag_next = 0;  // host mirror of the device tag base
   int64_t launches = 0;
   bool taps_on = false;
   long long *timeline_buf = nullptr;
@@ -120,7 +119,6 @@ int launch_iteration(bart_chain *h, int device_rng) {
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
   h->launches += 2;
-  h->tag_next += (uint64_t)(h->c.m + 1);
   h->iteration += 1;
   return BART_OK;
 }
@@ -193,7 +191,7 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   nblk = (int)((c.n + chunk - 1) / chunk);
   c.nblk = nblk;
   c.chunk = (int)chunk;
-  h->smem = sweep_smem_bytes(c.m, c.chunk);
+  h->smem = sweep_smem_bytes(c.m, c.chunk, c.size);
   if (sweep_words_per_thread(c.chunk) < 0 || (int64_t)h->smem > optin)
     return bail(fail(BART_EINVAL, "n per device too large for the smem-resident sweep: chunk " +
                                       std::to_string(chunk) + " points needs " + std::to_string(h->smem) +
@@ -209,10 +207,12 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   uint16_t *axis = nullptr;
   int32_t *mc = nullptr;
   uint32_t *ob = nullptr;
-  TreeMove *moves = nullptr;
+  uint8_t *recs = nullptr;
   TreeHdr *hdr = nullptr;
   double *rm = nullptr, *ra = nullptr, *rz = nullptr, *rc2 = nullptr, *s2 = nullptr, *s2d = nullptr;
-  unsigned long long *accum = nullptr, *itd = nullptr, *ctr = nullptr, *abase = nullptr;
+  unsigned long long *xacc = nullptr, *itd = nullptr, *xsnap = nullptr;
+  int *errf = nullptr;
+  unsigned long long *cacc = nullptr, *csnap = nullptr;
   cudaError_t e = cudaSuccess;
 #define OWN(ptr, cnt) \
   if (e == cudaSuccess) e = own(h, &ptr, cnt)
@@ -225,7 +225,8 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   OWN(leaf, (size_t)c.m * c.size);
   OWN(mc, (size_t)c.p);
   OWN(ob, (size_t)(c.p + 31) / 32);
-  OWN(moves, (size_t)c.m);
+  c.rstride = rec_stride(c.size);
+  OWN(recs, (size_t)c.m * c.rstride);
   OWN(hdr, (size_t)c.m);
   OWN(rm, (size_t)c.m * 5);
   OWN(ra, (size_t)c.m);
@@ -234,9 +235,11 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   OWN(s2, 1);
   OWN(s2d, 1);
   OWN(acc, (size_t)c.m);
-  OWN(accum, (size_t)(kSlotsMax + 1) * kAccWords);
-  OWN(abase, (size_t)(kSlotsMax + 1) * 5 + 16);
-  OWN(ctr, 16);  // counter alone on its 128-B line
+  OWN(xacc, (size_t)kXSets * kXSetWords);
+  OWN(xsnap, 1 + (size_t)kXSets * (kSlotsMax + 1) * 4);
+  OWN(errf, 32);
+  OWN(cacc, (size_t)kCSets * kCSetWords);
+  OWN(csnap, (size_t)kCSets * kCSetWords);
   OWN(itd, 1);
 #undef OWN
   if (e != cudaSuccess) return bail(fail(BART_ECUDA, std::string("allocation: ") + cudaGetErrorString(e)));
@@ -249,7 +252,7 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.leaf = leaf;
   c.max_cuts = mc;
   c.open_bits = ob;
-  c.moves = moves;
+  c.rec = recs;
   c.hdr = hdr;
   c.rand_move = rm;
   c.rand_acc = ra;
@@ -258,9 +261,16 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.sigma2 = s2;
   c.sigma2_draw = s2d;
   c.accepted = acc;
-  c.accum = accum;
-  c.accum_base = abase;
-  c.counter = ctr;
+  c.xacc = xacc;
+  c.xpeer[0] = xacc;
+  c.n_shards = 1;
+  c.nblk_total = c.nblk;
+  c.shard_sys = 0;
+  c.xsnap = xsnap;
+  c.err = errf;
+  c.cacc = cacc;
+  c.cpeer[0] = cacc;
+  c.csnap = csnap;
   c.iter_dev = itd;
 
   // predictors: (n, p) row-major -> (p, n_pad)
@@ -393,7 +403,6 @@ int bart_run(bart_chain *h, int64_t n_iter) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
       h->launches += 2;
-      h->tag_next += (uint64_t)(h->c.m + 1);
       h->iteration += 1;
     } else if (int rc = launch_iteration(h, 1)) {
       return rc;
@@ -454,7 +463,8 @@ int bart_get_proposals(bart_chain *h, int64_t *rows, double *struct_log) {
   if (int rc = bart_sync(h)) return rc;
   const int m = h->c.m;
   std::vector<TreeMove> mv(m);
-  CUDA_TRY(cudaMemcpy(mv.data(), h->c.moves, sizeof(TreeMove) * m, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy2D(mv.data(), sizeof(TreeMove), h->c.rec, (size_t)h->c.rstride, sizeof(TreeMove), m,
+                        cudaMemcpyDeviceToHost));
   for (int j = 0; j < m; ++j) {
     const TreeMove &t = mv[j];
     const int64_t vals[BART_PROPOSAL_ROWS] = {t.kind,    t.node,        t.axis,         t.cut,
@@ -486,8 +496,8 @@ int bart_set_timeline(bart_chain *h, int on) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
-  if (on && !h->timeline_buf) CUDA_TRY(own(h, &h->timeline_buf, (size_t)3 * (c.m + 1) * 8));
-  if (on && !h->trace_buf) CUDA_TRY(own(h, &h->trace_buf, (size_t)(c.m + 1) * c.nblk * 2));
+  if (on && !h->timeline_buf) CUDA_TRY(own(h, &h->timeline_buf, (size_t)3 * (c.m + 2) * 8));
+  if (on && !h->trace_buf) CUDA_TRY(own(h, &h->trace_buf, (size_t)(c.m + 2) * c.nblk * 2));
   c.timeline = on ? h->timeline_buf : nullptr;
   c.trace = on ? h->trace_buf : nullptr;
   if (h->graph) {
@@ -500,14 +510,14 @@ int bart_set_timeline(bart_chain *h, int on) {
 int bart_get_timeline(bart_chain *h, int64_t *out) {
   if (int rc = bart_sync(h)) return rc;
   if (!h->timeline_buf) return fail(BART_ESTATE, "timeline not enabled (bart_set_timeline)");
-  CUDA_TRY(cudaMemcpy(out, h->timeline_buf, (size_t)3 * (h->c.m + 1) * 8 * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->timeline_buf, (size_t)3 * (h->c.m + 2) * 8 * 8, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 
 int bart_get_trace(bart_chain *h, int64_t *out) {
   if (int rc = bart_sync(h)) return rc;
   if (!h->trace_buf) return fail(BART_ESTATE, "timeline not enabled (bart_set_timeline)");
-  CUDA_TRY(cudaMemcpy(out, h->trace_buf, (size_t)(h->c.m + 1) * h->c.nblk * 2 * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->trace_buf, (size_t)(h->c.m + 2) * h->c.nblk * 2 * 8, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 
@@ -681,7 +691,6 @@ int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
       h->launches += 2;
-      h->tag_next += (uint64_t)(h->c.m + 1);
       h->iteration += 1;
     } else if (int rc = launch_iteration(h, 1)) {
       return rc;
@@ -712,7 +721,6 @@ int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
     CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
     CUDA_TRY(cudaEventRecord(ev[3 + 3 * i], h->stream));
     h->launches += 2;
-    h->tag_next += (uint64_t)(h->c.m + 1);
     h->iteration += 1;
   }
   CUDA_TRY(cudaEventRecord(ev.back(), h->stream));

@@ -18,14 +18,24 @@ namespace bart {
 
 constexpr int kMaxDepth = 8;
 constexpr int kSlotsMax = 128;        // leaves of a depth-8 tree
-constexpr int kWorkers = 480;                 // threads that own points (15 warps)
+constexpr int kWorkers = 448;                 // threads that own points (14 warps)
 constexpr int kWorkWarps = kWorkers / 32;
-constexpr int kSweepThreads = kWorkers + 32;  // + one producer warp (TMA / stage loads)
+constexpr int kSweepThreads = kWorkers + 64;  // + control warp (exchange, decision) + helper warp
 constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr int kMaxCtas = 256;         // mailbox gather unroll bound
-constexpr int kGatherUnroll = kMaxCtas / 32;
+constexpr int kMaxCtas = 256;         // CTAs per shard (one per SM)
 constexpr int kProposeWarps = 4;
-constexpr int kAccWords = 8;       // per slot: 4 fixed-point limbs, 1 count, pad (64 B)
+constexpr int kMaxShards = 8;         // n-shards whose exchange words a sweep adds into
+// Exchange accumulators: kXSets sets (exchange X uses set X % kXSets), each
+// kSlotsMax+1 slot lines of kXLineWords u64 (128 B): 3 fixed-point limbs of
+// the slot's f64 residual sum, 1 point count, padding.
+constexpr int kXSets = 3;
+constexpr int kXLineWords = 16;
+constexpr size_t kXSetWords = (size_t)(kSlotsMax + 1) * kXLineWords;
+// Count channel: the per-leaf point counts of tree j (needed one exchange
+// before tree j's decision) travel through their own tagged words, set j % 4,
+// one u64 per slot, added and polled by the helper warps.
+constexpr int kCSets = 4;
+constexpr size_t kCSetWords = (size_t)kSlotsMax;
 
 enum : int { KIND_NONE = 0, KIND_GROW = 1, KIND_PRUNE = 2 };
 
@@ -35,17 +45,29 @@ struct HP {
   double depth_prob[kMaxDepth];
 };
 
-// One tree's proposal (sampler.py:263-306) plus the leaf list of the larger
-// tree of the move pair, which the sweep histograms over.
+// One tree's proposal (sampler.py:263-306) plus everything the sweep needs
+// about the tree, as one contiguous per-tree RECORD the sweep fetches with a
+// single TMA bulk copy: this header, then float old_leaf[size] (the tree's
+// leaf row before the sweep) and double z[size] (its leaf_z draws).
 struct __align__(16) TreeMove {
   int32_t kind, node, axis, cut;
   int32_t depth, n_axes, n_splits, w_small;
   int32_t w_prime_big, growable_big, gl, gr;
-  int32_t nslots, pad0;
+  int32_t nslots, pad0, pad1, pad2;
   double struct_log;
   double log_u;  // log(accept_u): lets the sweep decide without exp() off the near-tie band
-  uint8_t slot_node[kSlotsMax];
+  double acc_u;  // accept_u (sampler.py:833)
+  double pad3;
+  uint8_t slot_node[kSlotsMax];  // leaves of the larger tree of the move pair, heap order
 };
+static_assert(sizeof(TreeMove) == 224, "record header layout");
+
+__host__ __device__ __forceinline__ int rec_stride(int size) { return (224 + 12 * size + 15) & ~15; }
+__device__ __forceinline__ const TreeMove &rec_hdr(const uint8_t *rec) { return *reinterpret_cast<const TreeMove *>(rec); }
+__device__ __forceinline__ const float *rec_leaf(const uint8_t *rec) { return reinterpret_cast<const float *>(rec + 224); }
+__device__ __forceinline__ const double *rec_z(const uint8_t *rec, int size) {
+  return reinterpret_cast<const double *>(rec + 224 + 4 * size);
+}
 
 // Compact per-tree header the sweep keeps in shared memory for all trees.
 struct __align__(8) TreeHdr {
@@ -68,7 +90,8 @@ struct ChainDev {
   const int32_t *max_cuts;
   const uint32_t *open_bits;  // bit a set iff max_cuts[a] > 0
   int P_open;                 // popcount of open_bits
-  TreeMove *moves;
+  uint8_t *rec;   // (m, rec_stride(size)) per-tree records
+  int rstride;
   TreeHdr *hdr;
   double *rand_move, *rand_acc, *rand_z, *rand_chi2;
   double *sigma2, *sigma2_draw;
@@ -76,9 +99,17 @@ struct ChainDev {
   int64_t *tap_counts;
   double *tap_sums;
   int taps;
-  unsigned long long *accum;    // [kSlotsMax+1][kAccWords] monotonic fixed-point slot accumulators
-  unsigned long long *counter;  // monotonic exchange arrival counter (own 128-B line)
-  unsigned long long *accum_base;  // accumulator + counter values at the end of the last sweep
+  unsigned long long *xacc;     // this shard's exchange sets [kXSets][kXSetWords] (polled)
+  unsigned long long *xpeer[kMaxShards];  // every shard's xacc (own included): where partials are added
+  int n_shards;                 // copies in xpeer
+  int nblk_total;               // CTAs over all shards = arrival tag of a complete word
+  int shard_sys;                // 1: peers on other devices (system-scope fences)
+  int *err;                     // device error flags (bit 0: exchange value out of fixed-point range)
+  unsigned long long *xsnap;    // [1 + kXSets*(kSlotsMax+1)*4]: exchange count, then every polled
+                                // word's last complete value (the next sweep's baseline)
+  unsigned long long *cacc;     // this shard's count channel [kCSets][kCSetWords] (polled)
+  unsigned long long *cpeer[kMaxShards];  // every shard's cacc
+  unsigned long long *csnap;    // [kCSets*kCSetWords] last complete count words
   unsigned long long *iter_dev;
   uint64_t seed;
   int nblk, chunk;

@@ -10,7 +10,7 @@
 namespace bart {
 
 void launch_propose(const ChainDev &c, int device_rng, cudaStream_t s);
-size_t sweep_smem_bytes(int m, int chunk);
+size_t sweep_smem_bytes(int m, int chunk, int size);
 cudaError_t sweep_prepare(size_t smem);
 int sweep_max_ctas(size_t smem, int device, int chunk);
 int sweep_words_per_thread(int chunk);

@@ -112,6 +112,10 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
   const int j = blockIdx.x * kProposeWarps + wl;
   if (j >= c.m) return;
   const int D = c.D, half = c.half, size = c.size;
+  uint8_t *rec = c.rec + (size_t)j * c.rstride;
+  float *rec_old = reinterpret_cast<float *>(rec + 224);
+  double *rec_zz = reinterpret_cast<double *>(rec + 224 + 4 * size);
+  for (int h = lane; h < size; h += 32) rec_old[h] = c.leaf[(size_t)j * size + h];
   uint8_t *cut = s_cut[wl];
   uint16_t *ax = s_axis[wl];
   for (int i = lane; i < half; i += 32) {
@@ -144,12 +148,17 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
       double sn, cs;
       sincospi(2.0 * u2, &sn, &cs);
       c.rand_z[(size_t)j * size + 2 * q] = rad * cs;
-      if (2 * q + 1 < size) c.rand_z[(size_t)j * size + 2 * q + 1] = rad * sn;
+      rec_zz[2 * q] = rad * cs;
+      if (2 * q + 1 < size) {
+        c.rand_z[(size_t)j * size + 2 * q + 1] = rad * sn;
+        rec_zz[2 * q + 1] = rad * sn;
+      }
     }
   } else {
 #pragma unroll
     for (int k = 0; k < 5; ++k) u[k] = c.rand_move[(size_t)j * 5 + k];
     acc_u = c.rand_acc[j];
+    for (int h = lane; h < size; h += 32) rec_zz[h] = c.rand_z[(size_t)j * size + h];
   }
 
   // ---- candidate sets in heap order (sampler.py:342-360)
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
   }
 
   // ---- leaves of the larger tree, heap order: the sweep's histogram slots
-  TreeMove &mv = c.moves[j];
+  TreeMove &mv = *reinterpret_cast<TreeMove *>(rec);
   int nslots = 0, slot_l = 0, slot_r = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -318,6 +327,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
     mv.nslots = nslots;
     mv.struct_log = struct_log;
     mv.log_u = log(acc_u);
+    mv.acc_u = acc_u;
     TreeHdr hd;
     hd.kind = (uint8_t)kind;
     hd.node = (uint8_t)t;

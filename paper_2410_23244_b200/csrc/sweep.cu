@@ -10,83 +10,104 @@
 //   phase 11 update_caches              :737-761
 //   sigma    sigma2_draw/sum_squares    :790-799, 906-908
 //
-// Design (DESIGN.md §4).  One CTA per SM owns a contiguous chunk of points.
-// 15 worker warps hold the chunk's residuals and leaf indices in REGISTERS
-// for the whole sweep (4 points per 32-bit word, W words per thread) and run
-// one pass per tree: tree j-1's residual/cache update, tree j's per-leaf f64
-// residual sums, and tree j+1's grow refresh and leaf counts (counts one
-// tree early).  A 16th warp is the CTA's control warp: it streams each tree's
-// n-byte leaf-index row and split column into shared memory with TMA bulk
-// copies two trees ahead, publishes the CTA's partials, and decides.
+// Design (DESIGN.md §4.2).  One CTA per SM owns a contiguous chunk of points.
+// 14 worker warps hold the chunk's residuals (f32) and the larger-tree leaf
+// indices of trees e-1, e, e+1 (4 points per 32-bit word) in REGISTERS for the
+// whole sweep.  Per tree e the workers run
+//   A_e (critical path): tree e-1's residual update + cache write, then tree
+//       e's per-leaf f64 residual sums; publish the warp partials;
+//   B_e (hidden behind the exchange): tree e+2's grow refresh and per-leaf
+//       point counts, from its leaf-index row and split column that a TMA bulk
+//       copy staged in shared memory four trees ahead;
+// then wait for the decision of tree e.  The CONTROL warp folds the partials,
+// exchanges them across the grid and decides; nothing else sits on the
+// per-tree critical path.  The HELPER warp does everything that can lag one
+// tree behind: the next tree's count-only terms, one CTA's forest write per
+// tree, and the TMA prefetch of the per-tree data (cache row, split column and
+// the tree's record: proposal, leaf list, old leaf row, leaf draws).
 //
-// Cross-CTA reduction without a grid barrier or a decider: each CTA adds its
-// f64 partial, as an exact 64.64 fixed-point number split into 32-bit limbs,
-// into monotonic 64-bit accumulators with red.add (integer addition is
-// associative, so the total is bit-identical whatever the arrival order),
-// then bumps an arrival counter with red.release.  Every CTA acquires the
-// counter, reads the few accumulator words and, holding identical totals,
-// takes the same accept decision and leaf draws redundantly.  Count-only
-// terms of the ratio and draws are precomputed one tree early, so the
-// decision's critical path is one division per leaf.  m+2 exchanges per sweep.
+// Cross-CTA exchange without a grid barrier, counter, fence or decider: every
+// CTA adds its partials, as exact fixed point (3 x 37-bit limbs of a 111-bit
+// number with 64 fraction bits; counts as integers), into 64-bit words whose
+// top 16 bits count arrivals: each add is (1 << 48) | limb.  A reader knows
+// each word's last complete value, so a word is complete when (now - last)
+// carries exactly one arrival per CTA: the readers poll the data words
+// themselves, one L2 round trip after the last add lands.  Integer addition
+// is associative, so every CTA reads bit-identical totals and takes the same
+// decision redundantly.  Exchange X uses set X % 3; a CTA adds to X+3 only
+// after X+2 completed, which needs every CTA to have read X, so words never
+// need resetting.  The same words extend to n-sharding across GPUs
+// (DESIGN.md §6): a shard adds into every shard's copy (c.xpeer) and polls
+// its own.
 #include "common.cuh"
 #include "internal.h"
 
 namespace bart {
 
-constexpr int kRing = 3;  // TMA / stage ring depth: trees j, j+1, j+2
+constexpr int kRing = 4;  // trees e+1 .. e+4 staged
+constexpr int kTagShift = 48;
+constexpr unsigned long long kTagOne = 1ull << kTagShift;
+constexpr unsigned long long kDataMask = kTagOne - 1ull;
+constexpr int kLimbBits = 37;
+constexpr unsigned long long kLimbMask = (1ull << kLimbBits) - 1ull;
+constexpr int kPollSlots = (kSlotsMax + 1 + 31) / 32;  // slots per control lane
+constexpr int kCtrlWarp = kWorkWarps;  // then the helper warp
+
+// named barriers (0 is __syncthreads) and their thread counts
+enum : int { BAR_PARTIALS = 1, BAR_DECISION = 2, BAR_HREADY = 3, BAR_HDONE = 4, BAR_COUNTS = 5 };
+constexpr int kBarWC = kWorkers + 32;  // workers + control (PARTIALS, DECISION)
+constexpr int kBarWH = kWorkers + 32;  // workers + helper (COUNTS)
+constexpr int kBarCH = 64;             // control + helper (HREADY, HDONE)
 
 // count-only precomputation for one tree (see prepare())
 struct Prep {
-  unsigned long long cnt[kSlotsMax];
+  uint32_t cnt[kSlotsMax];
   double prec[kSlotsMax];  // tau_mu + n * tau
   double zs[kSlotsMax];    // z / sqrt(prec)
   double cadj[kSlotsMax];  // n * adj, the tree's own contribution to the sums
   double prec_l, prec_r, prec_p, zs_p, partial;
 };
 
-struct __align__(16) Stage {
-  double z[256];
-  float old_leaf[256];
-  uint8_t slot_node[kSlotsMax];
-  double struct_log;
-  double log_u;
-  double acc_u;
-  double pad;
+// decision outputs of one tree, read by the helper's bookkeeping
+struct Dec {
+  double v_s[kSlotsMax + 1];  // leaf draws (leaves of the larger tree, then the collapsed parent)
+  double sums_s[kSlotsMax];   // tree-excluded sums (taps)
+  int acc;
 };
 
 struct __align__(16) SweepSmem {
-  Stage stage[kRing];
   Prep prep[2];
-  double wsum[kSlotsMax][kWorkWarps];
-  uint32_t wcnt[kSlotsMax][kWorkWarps];
-  unsigned long long prev[kSlotsMax + 1][5];  // accumulator values after the last exchange
-  unsigned long long prev_counter;
-  double tot_sum[kSlotsMax];
-  unsigned long long tot_cnt[kSlotsMax];
-  double sums_s[kSlotsMax];   // tree-excluded sums of the decided tree (taps)
-  double q_s[kSlotsMax + 1];  // posterior means (leaves, then collapsed parent)
-  double v_s[kSlotsMax + 1];  // leaf draws
-  float row[256];             // new leaf row
-  float dlt[256];             // residual delta by larger-tree heap index
+  Dec dec[2];
+  double wsum[kWorkWarps][kSlotsMax];       // A pass: per-warp f64 sums of tree e
+  uint32_t wcnt[2][kWorkWarps][kSlotsMax];  // B pass: per-warp counts of tree e+2 (by parity)
+  double tot_sum[kSlotsMax + 1];            // exchange totals (control; slot 0 = sum r^2 at e = m)
+  uint32_t hcnt[kSlotsMax];                 // count-channel totals of the tree being prepared (helper)
+  double q_s[kSlotsMax + 1];                // posterior means (control scratch, wide trees)
+  float row[256];                           // new leaf row (helper scratch)
+  float dlt[256];                           // residual delta by larger-tree heap index
+  unsigned long long xprev[kXSets][kSlotsMax + 1][3];  // last complete value of every exchange word
+  unsigned long long cprev[kCSets][kCSetWords];       // last complete value of every count word
   unsigned long long mbar[kRing];
-  int flag_wr, flag_prune, flag_t, acc_e;
+  int flag_wr, flag_prune, flag_t;
 };
 
-size_t sweep_smem_bytes(int m, int chunk) {
+__host__ __device__ __forceinline__ size_t ring_slot_bytes(int chunk, int rstride) { return (size_t)2 * chunk + (size_t)rstride; }
+
+size_t sweep_smem_bytes(int m, int chunk, int size) {
   size_t b = sizeof(SweepSmem);
   b += ((size_t)m * sizeof(TreeHdr) + 15) & ~(size_t)15;
-  b += (size_t)chunk * 2 * kRing;  // leaf-index rows + split columns, ring of 3
+  b += (size_t)kRing * ring_slot_bytes(chunk, rec_stride(size));
   return b;
 }
 
 int sweep_words_per_thread(int chunk) {
   const int words = (chunk + 3) / 4;
-  for (int w : {1, 2, 4, 8, 16})
+  for (int w : {1, 2, 4, 8})
     if (w * kWorkers >= words) return w;
   return -1;
 }
 
-// ------------------------------------------------------------ async copies
+// ------------------------------------------------------------ async copies, barriers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *b) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
@@ -108,16 +129,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// timeline stamps: SM clock cycles (all stamps of one CTA share one clock)
+__device__ __forceinline__ long long gtimer() { return clock64(); }
+// cross-CTA trace stamps: the global nanosecond timer
+__device__ __forceinline__ long long nstimer() {
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  return (long long)g;
+}
 
 // ------------------------------------------------------------ byte-lane ops
 // refresh_leaf_indices on 4 points: L==t -> 2t + (x >= cut) (sampler.py:541-545)
@@ -140,6 +162,12 @@ __device__ __forceinline__ uint32_t collapse4(uint32_t l, uint32_t t) {
   }
   return out;
 }
+// 0x80 in every byte of a that equals the byte in b4 (SWAR zero-byte test)
+__device__ __forceinline__ uint32_t bytes_eq(uint32_t a, uint32_t b4) {
+  const uint32_t x = a ^ b4;
+  const uint32_t t = ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x;
+  return ~t & 0x80808080u;
+}
 
 __device__ __forceinline__ float4 update4(float4 r, uint32_t l, const float *dlt) {
   r.x = __fadd_rn(r.x, dlt[l & 0xffu]);
@@ -149,165 +177,310 @@ __device__ __forceinline__ float4 update4(float4 r, uint32_t l, const float *dlt
   return r;
 }
 
-struct PassArgs {
-  int nwords;
-  // tree e-1: residual update and cache write
-  bool do_update, wr_prev, prune_prev;
-  uint32_t t_prev;
-  uint32_t *gLprev;
-  // tree e: residual sums over its larger-tree indices (already refreshed)
-  const uint8_t *slots_cur;
-  int ns_cur;
-  // tree e+1: grow refresh of its cache row and point counts
-  bool has_next, grow_next;
-  const uint32_t *Lnext, *Xnext;
-  uint32_t t_next, cut_next;
-  const uint8_t *slots_next;
-  int ns_next;
+struct Geom {
+  int m, chunk, nwords, cta, nblk, size;
+  int64_t start;
+  uint32_t lenp;
+  uint32_t slot_bytes;  // ring slot: cache row | split column | record
+  uint8_t *ring;
+  TreeHdr *hdr;
+  __device__ __forceinline__ uint8_t *slot(int j) const { return ring + (size_t)(j % kRing) * slot_bytes; }
+  __device__ __forceinline__ const uint8_t *rec(int j) const { return slot(j) + 2 * (size_t)chunk; }
 };
 
-// One register pass over the chunk.  FIRST: tree e-1's update (residuals
-// f32, cache write) and tree e+1's grow refresh.  Every pass: for slot group
-// [base, base+NS) the f64 residual sums of tree e and the counts of tree e+1.
-// Counts one tree early let the decider precompute every count-only term of
-// the acceptance ratio and leaf draws off the critical path.
+// ------------------------------------------------------------ worker passes
+struct APass {
+  bool do_update, wr, prune;
+  uint32_t t;
+  uint32_t *gL;  // this chunk of tree e-1's global cache row
+  const uint8_t *slots;
+  int ns;
+};
+
+// A pass over the register-resident chunk for slot group [base, base+NS).
+// FIRST: tree e-1's update (residuals f32 with the reference's two roundings,
+// sampler.py:755-760; cache write of the final tree).  Then the f64 residual
+// sums of tree e over its larger-tree leaves (sampler.py:556-576).
 template <int W, int NS, bool FIRST>
-__device__ __forceinline__ void tree_pass(float4 (&r)[W], const uint32_t (&lbp)[W], const uint32_t (&lbc)[W],
-                                          uint32_t (&lbn)[W], const PassArgs &A, const float *dlt, SweepSmem &S,
-                                          int tid, int warp, int lane, int base) {
-  uint32_t sn[8], gn[8];
-  double acc[8];
-  uint32_t cnt[8];
+__device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
+                                          const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
+                                          int warp, int lane, int base) {
+  uint32_t sn[NS];
+  double acc[NS];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    sn[s] = (s < NS && base + s < A.ns_cur) ? A.slots_cur[base + s] : 0xffffu;
-    gn[s] = (s < NS && base + s < A.ns_next) ? A.slots_next[base + s] : 0xffffu;
+  for (int s = 0; s < NS; ++s) {
+    sn[s] = base + s < A.ns ? A.slots[base + s] : 0xffffu;
     acc[s] = 0.0;
-    cnt[s] = 0u;
   }
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     const int w = tid + k * kWorkers;
-    if (w < A.nwords) {
-      if (FIRST) {
-        if (A.do_update) {
-          r[k] = update4(r[k], lbp[k], dlt);
-          if (A.wr_prev) A.gLprev[w] = A.prune_prev ? collapse4(lbp[k], A.t_prev) : lbp[k];
-        }
-        if (A.has_next) {
-          uint32_t l = A.Lnext[w];
-          if (A.grow_next) l = grow4(l, A.Xnext[w], A.t_next, A.cut_next);
-          lbn[k] = l;
-        }
+    if (w < G.nwords) {
+      if (FIRST && A.do_update) {
+        r[k] = update4(r[k], lp[k], dlt);
+        if (A.wr) A.gL[w] = A.prune ? collapse4(lp[k], A.t) : lp[k];
       }
       const float rv[4] = {r[k].x, r[k].y, r[k].z, r[k].w};
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const uint32_t h = (lbc[k] >> (8 * b)) & 0xffu, g = (lbn[k] >> (8 * b)) & 0xffu;
+        const uint32_t h = (lc[k] >> (8 * b)) & 0xffu;
         const double v = (double)rv[b];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
+        for (int s = 0; s < NS; ++s)
           if (h == sn[s]) acc[s] = __dadd_rn(acc[s], v);
-          if (g == gn[s]) cnt[s] += 1u;
-        }
       }
     }
   }
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const double v = warp_sum_f64(acc[s]);
-    const uint32_t cc = __reduce_add_sync(0xffffffffu, cnt[s]);
-    if (lane == 0) {
-      S.wsum[base + s][warp] = v;
-      S.wcnt[base + s][warp] = cc;
-    }
+    if (lane == 0 && base + s < A.ns) S.wsum[warp][base + s] = v;
   }
 }
 
 template <int W>
-__device__ __forceinline__ void tree_passes(int nsx, float4 (&r)[W], const uint32_t (&lbp)[W],
-                                            const uint32_t (&lbc)[W], uint32_t (&lbn)[W], const PassArgs &A,
-                                            const float *dlt, SweepSmem &S, int tid, int warp, int lane) {
-  // slot-count variants limited to {2, 4, 8} (+ 8-wide follow-up passes) so
-  // that the code a tree executes stays inside the instruction cache
-  if (nsx <= 2)
-    tree_pass<W, 2, true>(r, lbp, lbc, lbn, A, dlt, S, tid, warp, lane, 0);
-  else if (nsx <= 4)
-    tree_pass<W, 4, true>(r, lbp, lbc, lbn, A, dlt, S, tid, warp, lane, 0);
+__device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
+                                            const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
+                                            int warp, int lane) {
+  // slot-count variants {2, 4, 8} (+ 8-wide follow-up passes) keep the code
+  // a tree executes inside the instruction cache
+  if (A.ns <= 2)
+    sums_pass<W, 2, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+  else if (A.ns <= 4)
+    sums_pass<W, 4, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
   else
-    tree_pass<W, 8, true>(r, lbp, lbc, lbn, A, dlt, S, tid, warp, lane, 0);
-  for (int base = 8; base < nsx; base += 8) tree_pass<W, 8, false>(r, lbp, lbc, lbn, A, dlt, S, tid, warp, lane, base);
+    sums_pass<W, 8, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+  for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+}
+
+// x >= cut per byte (unsigned), 0x01 in every byte where it holds: 9-bit
+// lanes so the subtraction's borrow lands in bit 8 of each lane
+__device__ __forceinline__ uint32_t bytes_geu(uint32_t x, uint32_t c4) {
+  const uint32_t de = ((x & 0x00ff00ffu) | 0x01000100u) - (c4 & 0x00ff00ffu);
+  const uint32_t dodd = (((x >> 8) & 0x00ff00ffu) | 0x01000100u) - ((c4 >> 8) & 0x00ff00ffu);
+  return ((de >> 8) & 0x00010001u) | (dodd & 0x01000100u);
+}
+// refresh_leaf_indices on 4 points (sampler.py:541-545), SWAR: bytes equal to
+// t become 2t + (x >= cut)
+__device__ __forceinline__ uint32_t grow4s(uint32_t l, uint32_t x, uint32_t t4, uint32_t c4, uint32_t b4) {
+  const uint32_t msk = (bytes_eq(l, t4) >> 7) * 0xffu;
+  return (l & ~msk) | (msk & (b4 | bytes_geu(x, c4)));
+}
+
+template <int W, int NS>
+__device__ __forceinline__ void count_pass(const uint32_t (&v)[W], const Geom &G, const uint8_t *slots, int ns,
+                                           int base, uint32_t *wrow, int tid, int lane) {
+  uint32_t cnt[NS], s4[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    s4[s] = base + s < ns ? 0x01010101u * (uint32_t)slots[base + s] : 0xffffffffu;
+    cnt[s] = 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const int w = tid + k * kWorkers;
+    if (w < G.nwords) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) cnt[s] += __popc(bytes_eq(v[k], s4[s]));
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t cc = __reduce_add_sync(0xffffffffu, cnt[s]);
+    if (lane == 0 && base + s < ns) wrow[base + s] = cc;
+  }
+}
+
+// B pass: grow refresh of tree j's cache row (staged in its ring slot) into
+// registers and the per-leaf point counts of its larger tree (sampler.py:
+// 541-553), reduced per warp into wrow.  Padding bytes are 0 and never match
+// a slot (heap indices >= 1); unused slot lanes compare against 0xff..ff,
+// which only a depth-8 index 255 could equal, and those lanes are not stored.
+template <int W>
+__device__ __forceinline__ void refresh_count(uint32_t (&out)[W], const uint8_t *slot, const Geom &G,
+                                              const TreeHdr hd, const uint8_t *slots, uint32_t *wrow, int tid,
+                                              int lane) {
+  const uint32_t *Lr = reinterpret_cast<const uint32_t *>(slot);
+  const uint32_t *Xr = reinterpret_cast<const uint32_t *>(slot + G.chunk);
+  const bool g = hd.kind == KIND_GROW;
+  const uint32_t t4 = 0x01010101u * hd.node, c4 = 0x01010101u * hd.cut, b4 = 0x01010101u * (2u * hd.node);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const int w = tid + k * kWorkers;
+    uint32_t l = 0u;
+    if (w < G.nwords) {
+      l = Lr[w];
+      if (g) l = grow4s(l, Xr[w], t4, c4, b4);
+    }
+    out[k] = l;
+  }
+  const int ns = hd.nslots;
+  if (ns <= 2)
+    count_pass<W, 2>(out, G, slots, ns, 0, wrow, tid, lane);
+  else if (ns <= 4)
+    count_pass<W, 4>(out, G, slots, ns, 0, wrow, tid, lane);
+  else
+    for (int base = 0; base < ns; base += 8) count_pass<W, 8>(out, G, slots, ns, base, wrow, tid, lane);
 }
 
 // ------------------------------------------------------------ exchange
-// f64 -> 64.64 fixed point, two's complement, as four 32-bit limbs.  Exact
-// for |x| >= 2^-12 with |x| < 2^63 (CTA partials); tinier values round at 2^-64.
-__device__ __forceinline__ void to_limbs(double x, unsigned long long (&l)[4]) {
+// f64 -> 111-bit two's-complement fixed point with 64 fraction bits, as three
+// 37-bit limbs.  Exact for 2^-12 <= |x| < 2^45; tinier values round at 2^-64.
+__device__ __forceinline__ void to_limbs(double x, unsigned long long (&l)[3], int *err) {
+  if (!(fabs(x) < 0x1.0p45)) {  // also catches NaN
+    if (err) atomicOr(err, 1);
+    x = 0.0;
+  }
   const long long hi = __double2ll_rd(x);
-  const double rem = __dsub_rn(x, (double)hi);  // exact, in [0, 1)
+  const double rem = __dsub_rn(x, (double)hi);  // exact, in [0, 1]
   const unsigned long long lo = __double2ull_rn(__dmul_rn(rem, 0x1.0p64));
-  l[0] = lo & 0xffffffffull;
-  l[1] = lo >> 32;
-  l[2] = (unsigned long long)hi & 0xffffffffull;
-  l[3] = (unsigned long long)hi >> 32;
+  l[0] = lo & kLimbMask;
+  l[1] = ((lo >> kLimbBits) | ((unsigned long long)hi << (64 - kLimbBits))) & kLimbMask;
+  l[2] = ((unsigned long long)(hi >> (2 * kLimbBits - 64))) & kLimbMask;
 }
 
-// accumulated limb deltas (mod 2^64 each) -> the f64 total (mod 2^128 value)
-__device__ __forceinline__ double from_limbs(const unsigned long long (&d)[4]) {
-  unsigned long long lo = d[0], hi = 0;
-  unsigned long long t = d[1] << 32;
-  lo += t;
-  hi += (lo < t) + (d[1] >> 32);
-  hi += d[2] + (d[3] << 32);
-  const bool neg = (long long)hi < 0;
-  if (neg) {  // negate the 128-bit value
+// limb sums (each < 2^48) -> f64 of the 111-bit total
+__device__ __forceinline__ double from_limbs(unsigned long long t0, unsigned long long t1, unsigned long long t2) {
+  unsigned long long lo = t0, hi = 0;
+  const unsigned long long a = t1 << kLimbBits;
+  lo += a;
+  hi += (lo < a ? 1ull : 0ull) + (t1 >> (64 - kLimbBits));
+  hi += t2 << (2 * kLimbBits - 64);
+  hi &= (1ull << 47) - 1ull;  // mod 2^111
+  const bool neg = (hi >> 46) & 1ull;
+  if (neg) {  // magnitude = 2^111 - V
     lo = ~lo + 1ull;
-    hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+    hi = (~hi + (lo == 0ull ? 1ull : 0ull)) & ((1ull << 47) - 1ull);
   }
   const double mag = __dadd_rn(__dmul_rn((double)hi, 0x1.0p64), (double)lo);
   const double v = __dmul_rn(mag, 0x1.0p-64);
   return neg ? -v : v;
 }
 
-// Control warp: fold the worker warps' partials of nsx slots (fixed order),
-// add them into the accumulators, release the arrival, wait for every CTA,
-// and read back the totals (sums, counts) of this exchange.
-__device__ __forceinline__ void exchange(const ChainDev &c, SweepSmem &S, int nsx, unsigned long long target,
-                                         int lane) {
-  for (int s = lane; s < nsx; s += 32) {
-    double v = 0.0;
+__device__ __forceinline__ void red_add(unsigned long long *p, unsigned long long v, bool sys) {
+  if (sys)
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void ld_poll2(const unsigned long long *p, unsigned long long &a, unsigned long long &b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Control warp, exchange X: fold the worker warps' f64 partials of ns slots
+// (fixed order), add them as fixed-point limbs into every shard's copy of set
+// X % 3.  exchange_poll then waits until every word of the local copy carries
+// one more arrival per CTA than its last complete value; lane s returns the
+// total of slot s (and s + 32, ... in tot[]).
+__device__ __forceinline__ void exchange_add(const ChainDev &c, const SweepSmem &S, int ns, int set, int lane) {
+  const bool sys = c.shard_sys != 0;
+  const size_t set_off = (size_t)set * kXSetWords;
+  for (int s = lane; s < ns; s += 32) {
+    double w[kWorkWarps];
+#pragma unroll
+    for (int k = 0; k < kWorkWarps; ++k) w[k] = S.wsum[k][s];
+#pragma unroll
+    for (int step = 1; step < kWorkWarps; step <<= 1)  // fixed pairwise order
+#pragma unroll
+      for (int k = 0; k + step < kWorkWarps; k += 2 * step) w[k] = __dadd_rn(w[k], w[k + step]);
+    unsigned long long l[3];
+    to_limbs(w[0], l, c.err);
+    for (int g = 0; g < c.n_shards; ++g) {
+      unsigned long long *a = c.xpeer[g] + set_off + (size_t)s * kXLineWords;
+      red_add(a + 0, kTagOne | l[0], sys);
+      red_add(a + 1, kTagOne | l[1], sys);
+      red_add(a + 2, kTagOne | l[2], sys);
+    }
+  }
+}
+
+__device__ __forceinline__ void ld_poll1(const unsigned long long *p, unsigned long long &a) {
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_poll1s(const unsigned long long *p, unsigned long long &a) {
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ void exchange_poll(const ChainDev &c, SweepSmem &S, int ns, int set, int lane,
+                                              double (&tot)[kPollSlots]) {
+  const bool sys = c.shard_sys != 0;
+  const unsigned long long target = (unsigned long long)c.nblk_total << kTagShift;
+  const unsigned long long *base = c.xacc + (size_t)set * kXSetWords;
+  unsigned long long w[kPollSlots][3];
+  bool done;
+  do {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < kPollSlots; ++i) {
+      const int s = lane + 32 * i;
+      if (s < ns) {
+        const unsigned long long *a = base + (size_t)s * kXLineWords;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          if (sys)
+            ld_poll1s(a + k, w[i][k]);
+          else
+            ld_poll1(a + k, w[i][k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ok = ok && ((w[i][k] - S.xprev[set][s][k]) & ~kDataMask) == target;
+      }
+    }
+    done = __all_sync(0xffffffffu, ok);
+  } while (!done);
+#pragma unroll
+  for (int i = 0; i < kPollSlots; ++i) {
+    const int s = lane + 32 * i;
+    tot[i] = 0.0;
+    if (s < ns) {
+      unsigned long long d[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        d[k] = (w[i][k] - S.xprev[set][s][k]) & kDataMask;
+        S.xprev[set][s][k] = w[i][k];
+      }
+      tot[i] = from_limbs(d[0], d[1], d[2]);
+    }
+  }
+}
+
+// Helper warp, count channel: add this CTA's per-leaf counts of tree j into
+// every shard's copy of count set j % 4 / poll the local copy until complete.
+__device__ __forceinline__ void counts_add(const ChainDev &c, const SweepSmem &S, int j, int ns, int lane) {
+  const bool sys = c.shard_sys != 0;
+  const size_t off = (size_t)(j % kCSets) * kCSetWords;
+  for (int s = lane; s < ns; s += 32) {
     uint32_t cn = 0;
 #pragma unroll
-    for (int w = 0; w < kWorkWarps; ++w) {
-      v = __dadd_rn(v, S.wsum[s][w]);
-      cn += S.wcnt[s][w];
-    }
-    unsigned long long l[4];
-    to_limbs(v, l);
-    unsigned long long *a = c.accum + (size_t)s * kAccWords;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a + k), "l"(l[k]) : "memory");
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a + 4), "l"((unsigned long long)cn) : "memory");
+    for (int k = 0; k < kWorkWarps; ++k) cn += S.wcnt[j & 1][k][s];
+    for (int g = 0; g < c.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | (unsigned long long)cn, sys);
   }
-  __syncwarp();
-  if (lane == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(c.counter) : "memory");
-  unsigned long long v;
-  do {
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c.counter) : "memory");
-  } while (v < target);
-  for (int s = lane; s < nsx; s += 32) {
-    const unsigned long long *a = c.accum + (size_t)s * kAccWords;
-    unsigned long long now[5], d[4];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(now[k]) : "l"(a + k) : "memory");
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      d[k] = now[k] - S.prev[s][k];
-      S.prev[s][k] = now[k];
+}
+
+__device__ __forceinline__ void counts_poll(const ChainDev &c, SweepSmem &S, int j, int ns, int lane) {
+  const bool sys = c.shard_sys != 0;
+  const unsigned long long target = (unsigned long long)c.nblk_total << kTagShift;
+  const int set = j % kCSets;
+  const unsigned long long *base = c.cacc + (size_t)set * kCSetWords;
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int s = s0 + lane;
+    unsigned long long v = 0;
+    bool done;
+    do {
+      bool ok = true;
+      if (s < ns) {
+        if (sys)
+          ld_poll1s(base + s, v);
+        else
+          ld_poll1(base + s, v);
+        ok = ((v - S.cprev[set][s]) & ~kDataMask) == target;
+      }
+      done = __all_sync(0xffffffffu, ok);
+    } while (!done);
+    if (s < ns) {
+      S.hcnt[s] = (uint32_t)((v - S.cprev[set][s]) & kDataMask);
+      S.cprev[set][s] = v;
     }
-    S.tot_sum[s] = from_limbs(d);
-    S.tot_cnt[s] = now[4] - S.prev[s][4];
-    S.prev[s][4] = now[4];
   }
   __syncwarp();
 }
@@ -319,61 +492,67 @@ struct DecConst {
 
 __device__ __forceinline__ bool is_child(int h, int t, bool move) { return move && h >= 2 && (h >> 1) == t; }
 
-// Count-only terms of tree j, from the counts gathered one exchange early
-// (every CTA's control warp, off the critical path).  Same operations, in the
-// same order, as the reference: prec = tau_mu + n*tau, z/sqrt(prec)
-// (sampler.py:579-595), adjustment n*adj (sampler.py:575-576), and the count
-// part of the ratio (sampler.py:669-684).
-__device__ __forceinline__ void prepare(SweepSmem &S, Prep &P, const Stage &st, const TreeHdr hd, int lane,
-                                     const DecConst &K) {
+// Helper warp: count-only terms of tree j, from the counts the previous
+// exchange delivered.  Same operations, in the same order, as the reference:
+// prec = tau_mu + n*tau, z/sqrt(prec) (sampler.py:579-595), adjustment n*adj
+// (sampler.py:575-576), and the count part of the ratio (sampler.py:669-684).
+__device__ __forceinline__ void prepare(Prep &P, const uint32_t *tot_cnt, const uint8_t *rec, int size,
+                                        const TreeHdr hd, int lane, const DecConst &K) {
+  const TreeMove &mv = rec_hdr(rec);
+  const float *old_leaf = rec_leaf(rec);
+  const double *z = rec_z(rec, size);
   const int kind = hd.kind, t = hd.node, ns = hd.nslots;
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
   for (int j = lane; j < ns; j += 32) {
-    const int h = st.slot_node[j];
-    const unsigned long long cn = S.tot_cnt[j];
-    const float a32 = (grow && is_child(h, t, move)) ? st.old_leaf[t] : st.old_leaf[h];
+    const int h = mv.slot_node[j];
+    const uint32_t cn = tot_cnt[j];
+    const float a32 = (grow && is_child(h, t, move)) ? old_leaf[t] : old_leaf[h];
     const double prec = __dadd_rn(K.tau_mu, __dmul_rn((double)cn, K.tau));
     P.cnt[j] = cn;
     P.cadj[j] = __dmul_rn((double)cn, (double)a32);
     P.prec[j] = prec;
-    P.zs[j] = __ddiv_rn(st.z[h], __dsqrt_rn(prec));
+    P.zs[j] = __ddiv_rn(z[h], __dsqrt_rn(prec));
   }
   __syncwarp();
   if (move && lane < 2) {
-    const unsigned long long nl = P.cnt[hd.slot_l], nr = P.cnt[hd.slot_r];
+    const uint32_t nl = P.cnt[hd.slot_l], nr = P.cnt[hd.slot_r];
     const double prec_l = P.prec[hd.slot_l], prec_r = P.prec[hd.slot_r];
     const double prec_p = __dadd_rn(K.tau_mu, __dmul_rn((double)(nl + nr), K.tau));
     if (lane == 0) {
       P.prec_l = prec_l;
       P.prec_r = prec_r;
       P.prec_p = prec_p;
-      P.zs_p = __ddiv_rn(st.z[t], __dsqrt_rn(prec_p));
+      P.zs_p = __ddiv_rn(z[t], __dsqrt_rn(prec_p));
     } else {
       const double q = __ddiv_rn(__dmul_rn(K.tau_mu, prec_p), __dmul_rn(prec_l, prec_r));
-      P.partial = __dadd_rn(st.struct_log, __dsub_rn(__dmul_rn(0.5, log(q)), K.lm_term));
+      P.partial = __dadd_rn(mv.struct_log, __dsub_rn(__dmul_rn(0.5, log(q)), K.lm_term));
     }
   }
   __syncwarp();
 }
 
-// Phases 8-10 of tree e, on every CTA's control warp (critical path):
-// tree-excluded sums, posterior means (one division each), the acceptance
-// test and the residual delta per leaf of the larger tree.
-__device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, const Stage &st, const TreeHdr hd, int lane,
-                                       const DecConst &K) {
+// Control warp, phases 8-10 of tree e (critical path): tree-excluded sums,
+// posterior means (one division each), the acceptance test and the residual
+// delta per leaf of the larger tree.
+__device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, Dec &Do, const uint8_t *rec, const TreeHdr hd,
+                                       int lane, const DecConst &K) {
+  const TreeMove &mv = rec_hdr(rec);
+  const float *old_leaf = rec_leaf(rec);
   const int kind = hd.kind, t = hd.node, ns = hd.nslots;
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
-  for (int j = lane; j < ns; j += 32) S.sums_s[j] = __dadd_rn(S.tot_sum[j], P.cadj[j]);  // sampler.py:570-576
-  __syncwarp();
-  const double sl = move ? S.sums_s[hd.slot_l] : 0.0, sr = move ? S.sums_s[hd.slot_r] : 0.0;
+  const int sl_i = hd.slot_l, sr_i = hd.slot_r;
   for (int base = 0; base <= ns; base += 32) {
     const int j = base + lane;
     double num = 1.0, den = 1.0, zs = 0.0;
     if (j < ns) {
-      num = __dadd_rn(K.prior, __dmul_rn(K.tau, S.sums_s[j]));
+      const double sums = __dadd_rn(S.tot_sum[j], P.cadj[j]);  // sampler.py:570-576
+      Do.sums_s[j] = sums;
+      num = __dadd_rn(K.prior, __dmul_rn(K.tau, sums));
       den = P.prec[j];
       zs = P.zs[j];
-    } else if (j == ns && move) {  // the collapsed parent: count nl+nr, sum sl+sr
+    } else if (j == ns && move) {  // the collapsed parent: count nl+nr, sum sl+sr (sampler.py:861-866)
+      const double sl = __dadd_rn(S.tot_sum[sl_i], P.cadj[sl_i]);
+      const double sr = __dadd_rn(S.tot_sum[sr_i], P.cadj[sr_i]);
       num = __dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr)));
       den = P.prec_p;
       zs = P.zs_p;
@@ -381,14 +560,14 @@ __device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, const Stage 
     const double q = __ddiv_rn(num, den);
     if (j <= ns) {
       S.q_s[j] = q;
-      S.v_s[j] = __dadd_rn(q, zs);
+      Do.v_s[j] = __dadd_rn(q, zs);
     }
   }
   __syncwarp();
   int acc = 0;
   if (move && lane == 0) {
     // sum part (sampler.py:634-645): mean*mean*prec with the leaf posterior means
-    const double ml = S.q_s[hd.slot_l], mr = S.q_s[hd.slot_r], mp = S.q_s[ns];
+    const double ml = S.q_s[sl_i], mr = S.q_s[sr_i], mp = S.q_s[ns];
     const double tl = __dmul_rn(__dmul_rn(ml, ml), P.prec_l);
     const double tr = __dmul_rn(__dmul_rn(mr, mr), P.prec_r);
     const double tp = __dmul_rn(__dmul_rn(mp, mp), P.prec_p);
@@ -399,44 +578,149 @@ __device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, const Stage 
     // the reference's exp comparison is evaluated as written
     if (la >= 0.0)
       acc = 1;
-    else if (la < st.log_u - 1e-9)
+    else if (la < mv.log_u - 1e-9)
       acc = 0;
-    else if (la > st.log_u + 1e-9)
+    else if (la > mv.log_u + 1e-9)
       acc = 1;
     else
-      acc = st.acc_u < exp(la);
+      acc = mv.acc_u < exp(la);
   }
   acc = __shfl_sync(0xffffffffu, acc, 0);
   const bool fsmall = move && ((acc != 0) != grow);  // sampler.py:861
-  const float v_par = __double2float_rn(S.v_s[ns]);
+  const float v_par = __double2float_rn(Do.v_s[ns]);
   // residual delta per leaf of the larger tree (sampler.py:755-760)
   for (int j = lane; j < ns; j += 32) {
-    const int h = st.slot_node[j];
+    const int h = mv.slot_node[j];
     const bool child = is_child(h, t, move);
     const int oi = (grow && child) ? t : h;
-    const float nv = (fsmall && child) ? v_par : __double2float_rn(S.v_s[j]);
-    S.dlt[h] = __fsub_rn(st.old_leaf[oi], nv);
+    const float nv = (fsmall && child) ? v_par : __double2float_rn(Do.v_s[j]);
+    S.dlt[h] = __fsub_rn(old_leaf[oi], nv);
   }
   if (lane == 0) {
     S.flag_wr = acc;
     S.flag_prune = acc && !grow;
     S.flag_t = t;
-    S.acc_e = acc;
+    Do.acc = acc;
   }
   __syncwarp();
 }
 
-// CTA 0's bookkeeping for tree e, off the critical path: accept flag,
-// structure write, the new leaf row (final leaves keep their draw, other
-// slots a signed zero; sampler.py:836-848, 868-870) and the parity taps.
-__device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, const Prep &P, const Stage &st,
-                                         const TreeHdr hd, int e, int lane, const DecConst &K) {
+// The same decision with lane s holding slot s in registers (trees whose
+// larger tree has <= 31 leaves: every depth <= 5 tree and nearly every depth-6
+// one).  Identical operations and order to decide(); the per-slot inputs are
+// loaded before the exchange completes, so after the poll the critical path
+// is one division, three shuffles and the ratio.
+struct DecIn {
+  double cadj, den, zs, cadj_l, cadj_r;
+  float oldv;
+  int h;
+  bool child;
+  // lane 0
+  double prec_l, prec_r, prec_p, partial, log_u, acc_u;
+};
+
+__device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8_t *rec, const TreeHdr hd, int lane) {
+  const TreeMove &mv = rec_hdr(rec);
+  const float *old_leaf = rec_leaf(rec);
+  const int kind = hd.kind, t = hd.node, ns = hd.nslots;
+  const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
+  I.cadj = 0.0;
+  I.den = 1.0;
+  I.zs = 0.0;
+  I.cadj_l = I.cadj_r = 0.0;
+  I.oldv = 0.f;
+  I.h = 0;
+  I.child = false;
+  if (lane < ns) {
+    I.cadj = P.cadj[lane];
+    I.den = P.prec[lane];
+    I.zs = P.zs[lane];
+    I.h = mv.slot_node[lane];
+    I.child = is_child(I.h, t, move);
+    I.oldv = old_leaf[(grow && I.child) ? t : I.h];
+  } else if (lane == ns && move) {
+    I.cadj_l = P.cadj[hd.slot_l];
+    I.cadj_r = P.cadj[hd.slot_r];
+    I.den = P.prec_p;
+    I.zs = P.zs_p;
+  }
+  if (lane == 0) {
+    I.prec_l = P.prec_l;
+    I.prec_r = P.prec_r;
+    I.prec_p = P.prec_p;
+    I.partial = P.partial;
+    I.log_u = mv.log_u;
+    I.acc_u = mv.acc_u;
+  }
+}
+
+__device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &I, double tot, const TreeHdr hd,
+                                            int lane, const DecConst &K) {
+  const int kind = hd.kind, t = hd.node, ns = hd.nslots;
+  const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
+  const int sl_i = hd.slot_l, sr_i = hd.slot_r;
+  const double tl = __shfl_sync(0xffffffffu, tot, sl_i), tr = __shfl_sync(0xffffffffu, tot, sr_i);
+  double num = 1.0, sums = 0.0;
+  if (lane < ns) {
+    sums = __dadd_rn(tot, I.cadj);  // sampler.py:570-576
+    num = __dadd_rn(K.prior, __dmul_rn(K.tau, sums));
+  } else if (lane == ns && move) {  // the collapsed parent (sampler.py:861-866)
+    const double sl = __dadd_rn(tl, I.cadj_l), sr = __dadd_rn(tr, I.cadj_r);
+    num = __dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr)));
+  }
+  const double q = __ddiv_rn(num, I.den);
+  const double v = __dadd_rn(q, I.zs);
+  const double ml = __shfl_sync(0xffffffffu, q, sl_i), mr = __shfl_sync(0xffffffffu, q, sr_i);
+  const double mp = __shfl_sync(0xffffffffu, q, ns), vp = __shfl_sync(0xffffffffu, v, ns);
+  int acc = 0;
+  if (move && lane == 0) {  // sum part (sampler.py:634-645) and the test (sampler.py:833-834)
+    const double t_l = __dmul_rn(__dmul_rn(ml, ml), I.prec_l);
+    const double t_r = __dmul_rn(__dmul_rn(mr, mr), I.prec_r);
+    const double t_p = __dmul_rn(__dmul_rn(mp, mp), I.prec_p);
+    const double sum_part = __dmul_rn(0.5, __dsub_rn(__dadd_rn(t_l, t_r), t_p));
+    const double la = __dmul_rn(grow ? 1.0 : -1.0, __dadd_rn(I.partial, sum_part));
+    if (la >= 0.0)
+      acc = 1;
+    else if (la < I.log_u - 1e-9)
+      acc = 0;
+    else if (la > I.log_u + 1e-9)
+      acc = 1;
+    else
+      acc = I.acc_u < exp(la);
+  }
+  acc = __shfl_sync(0xffffffffu, acc, 0);
+  const bool fsmall = move && ((acc != 0) != grow);
+  if (lane < ns) {  // residual delta (sampler.py:755-760)
+    const float nv = (fsmall && I.child) ? __double2float_rn(vp) : __double2float_rn(v);
+    S.dlt[I.h] = __fsub_rn(I.oldv, nv);
+  }
+  if (lane == 0) {
+    S.flag_wr = acc;
+    S.flag_prune = acc && !grow;
+    S.flag_t = t;
+  }
+  __syncwarp();
+  named_arrive(BAR_DECISION, kBarWC);
+  // for the helper's bookkeeping (off the critical path)
+  if (lane < ns) Do.sums_s[lane] = sums;
+  if (lane <= ns) Do.v_s[lane] = v;
+  if (lane == 0) Do.acc = acc;
+}
+
+// Helper warp, one CTA per tree: accept flag, structure write, the new leaf
+// row (final leaves keep their draw, other slots a signed zero; sampler.py:
+// 836-848, 868-870) and the parity taps.
+__device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, const Prep &P, const Dec &Di,
+                                            const uint8_t *rec, const TreeHdr hd, int e, int lane,
+                                            const DecConst &K) {
+  const TreeMove &mv = rec_hdr(rec);
+  const double *z = rec_z(rec, c.size);
   const int size = c.size, half = c.half;
   const int kind = hd.kind, t = hd.node, ns = hd.nslots;
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
-  const int acc = S.acc_e;
+  const int acc = Di.acc;
   const bool fsmall = move && ((acc != 0) != grow);
-  const float v_par = __double2float_rn(S.v_s[ns]);
+  const float v_par = __double2float_rn(Di.v_s[ns]);
   if (lane == 0) {
     c.accepted[e] = (uint8_t)acc;
     if (acc) {
@@ -447,17 +731,17 @@ __device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, con
   for (int h = lane; h < size; h += 32) {
     float z0;
     if (K.prior == 0.0) {
-      z0 = copysignf(0.0f, (float)st.z[h]);  // 0 + z/sqrt(tau_mu) has the sign of z
+      z0 = copysignf(0.0f, (float)z[h]);  // 0 + z/sqrt(tau_mu) has the sign of z
     } else {
-      const double v0 = __dadd_rn(__ddiv_rn(K.prior, K.tau_mu), __ddiv_rn(st.z[h], __dsqrt_rn(K.tau_mu)));
+      const double v0 = __dadd_rn(__ddiv_rn(K.prior, K.tau_mu), __ddiv_rn(z[h], __dsqrt_rn(K.tau_mu)));
       z0 = __double2float_rn(__dmul_rn(v0, 0.0));
     }
     S.row[h] = z0;
   }
   __syncwarp();
   for (int j = lane; j < ns; j += 32) {
-    const int h = st.slot_node[j];
-    if (!(fsmall && is_child(h, t, move))) S.row[h] = __double2float_rn(S.v_s[j]);
+    const int h = mv.slot_node[j];
+    if (!(fsmall && is_child(h, t, move))) S.row[h] = __double2float_rn(Di.v_s[j]);
   }
   if (lane == 0 && fsmall) S.row[t] = v_par;
   __syncwarp();
@@ -469,97 +753,61 @@ __device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, con
     }
     __syncwarp();
     for (int j = lane; j < ns; j += 32) {
-      const int h = st.slot_node[j];
+      const int h = mv.slot_node[j];
       c.tap_counts[(size_t)e * size + h] = (int64_t)P.cnt[j];
-      c.tap_sums[(size_t)e * size + h] = S.sums_s[j];
+      c.tap_sums[(size_t)e * size + h] = Di.sums_s[j];
     }
   }
   __syncwarp();
 }
 
-// ------------------------------------------------------------ the kernel
-__device__ __forceinline__ void stage_load(const ChainDev &c, Stage &st, int j, int lane) {
-  const int size = c.size;
-  for (int h = lane; h < size; h += 32) {
-    cp_async8(&st.z[h], c.rand_z + (size_t)j * size + h);
-    cp_async4(&st.old_leaf[h], c.leaf + (size_t)j * size + h);
-  }
-  cp_async4(reinterpret_cast<uint32_t *>(st.slot_node) + lane,
-            reinterpret_cast<const uint32_t *>(c.moves[j].slot_node) + lane);
-  if (lane == 0) {
-    cp_async8(&st.struct_log, &c.moves[j].struct_log);
-    cp_async8(&st.log_u, &c.moves[j].log_u);
-    cp_async8(&st.acc_u, c.rand_acc + j);
-  }
-  cp_async_commit();
-}
-
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-struct Geom {
-  int m, chunk, nwords, cta, nblk;
-  int64_t start;
-  uint32_t lenp;
-  uint8_t *ring;
-  TreeHdr *hdr;
-};
-
-// Worker warps: the register-resident point chunk, one pass per exchange.
+// ------------------------------------------------------------ warp roles
+// Worker warps: the register-resident point chunk, one A and one B pass per tree.
 template <int W>
 __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int tid, int warp, int lane,
                                             long long *tl) {
   float4 r[W];
-  uint32_t lbp[W], lbc[W], lbn[W];  // larger-tree indices of trees e-1, e, e+1
+  uint32_t lp[W], lc[W], ln[W];  // larger-tree indices of trees e-1, e, e+1
   const float4 *gr4 = reinterpret_cast<const float4 *>(c.r + G.start);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     const int w = tid + k * kWorkers;
     r[k] = w < G.nwords ? gr4[w] : make_float4(0.f, 0.f, 0.f, 0.f);
-    lbp[k] = lbc[k] = lbn[k] = 0u;
+    lp[k] = lc[k] = ln[k] = 0u;
   }
-  __syncthreads();  // prologue barrier (control warp: ring and stages 0, 1 issued)
+  __syncthreads();  // prologue barrier (mbarriers initialised, trees 0..3 in flight)
   const int m = G.m;
+  if (m > 0) {  // tree 0: refresh + counts
+    mbar_wait(&S.mbar[0], 0u);
+    refresh_count<W>(ln, G.slot(0), G, G.hdr[0], rec_hdr(G.rec(0)).slot_node, S.wcnt[0][warp], tid, lane);
+    named_arrive(BAR_COUNTS, kBarWH);
+  }
   for (int e = -1; e <= m; ++e) {
-    const bool has_cur = e >= 0 && e < m, has_next = e + 1 < m;
-    const int ns_cur = has_cur ? G.hdr[e].nslots : 0, ns_next = has_next ? G.hdr[e + 1].nslots : 0;
-    if (tl && e >= 0) tl[(size_t)e * 8 + 0] = clock64();
-    PassArgs A;
-    A.nwords = G.nwords;
-    A.do_update = e > 0;
-    A.wr_prev = e > 0 && S.flag_wr;
-    A.prune_prev = e > 0 && S.flag_prune;
-    A.t_prev = (uint32_t)S.flag_t;
-    A.gLprev = reinterpret_cast<uint32_t *>(c.L + (size_t)(e > 0 ? e - 1 : 0) * c.n_pad + G.start);
-    A.ns_cur = ns_cur;
-    A.slots_cur = has_cur ? S.stage[e % kRing].slot_node : S.stage[0].slot_node;
-    A.has_next = has_next;
-    A.ns_next = ns_next;
-    A.slots_next = A.slots_cur;
-    if (has_next) {
-      const TreeHdr hn = G.hdr[e + 1];
-      const uint8_t *slot = G.ring + (size_t)((e + 1) % kRing) * 2 * G.chunk;
-      A.Lnext = reinterpret_cast<const uint32_t *>(slot);
-      A.Xnext = reinterpret_cast<const uint32_t *>(slot + G.chunk);
-      A.grow_next = hn.kind == KIND_GROW;
-      A.t_next = hn.node;
-      A.cut_next = hn.cut;
-      A.slots_next = S.stage[(e + 1) % kRing].slot_node;
-      mbar_wait(&S.mbar[(e + 1) % kRing], (uint32_t)(((e + 1) / kRing) & 1));
-    }
-    if (tl && e >= 0) tl[(size_t)e * 8 + 1] = clock64();
-    if (e < m) {
-      const int nsx = ns_cur > ns_next ? ns_cur : ns_next;
-      tree_passes<W>(nsx, r, lbp, lbc, lbn, A, S.dlt, S, tid, warp, lane);
-    } else {  // tree m-1's update, residual write-back, sum of squares (sampler.py:790-794)
+    if (tl) tl[(size_t)(e + 1) * 8 + 0] = gtimer();
+    // ---- A_e: critical path
+    if (e >= 0 && e < m) {
+      APass A;
+      A.do_update = e > 0;
+      A.wr = e > 0 && S.flag_wr;
+      A.prune = e > 0 && S.flag_prune;
+      A.t = (uint32_t)S.flag_t;
+      A.gL = reinterpret_cast<uint32_t *>(c.L + (size_t)(e > 0 ? e - 1 : 0) * c.n_pad + G.start);
+      A.slots = rec_hdr(G.rec(e)).slot_node;
+      A.ns = G.hdr[e].nslots;
+      sums_passes<W>(r, lp, lc, A, G, S.dlt, S, tid, warp, lane);
+      named_arrive(BAR_PARTIALS, kBarWC);
+    } else if (e == m) {  // tree m-1's update, residual write-back, sum of squares (sampler.py:790-794)
+      const bool wr = m > 0 && S.flag_wr, prune = S.flag_prune;
+      const uint32_t t = (uint32_t)S.flag_t;
+      uint32_t *gL = reinterpret_cast<uint32_t *>(c.L + (size_t)(m > 0 ? m - 1 : 0) * c.n_pad + G.start);
       float4 *out = reinterpret_cast<float4 *>(c.r + G.start);
       double ss = 0.0;
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         const int w = tid + k * kWorkers;
         if (w < G.nwords) {
-          r[k] = update4(r[k], lbp[k], S.dlt);
-          if (A.wr_prev) A.gLprev[w] = A.prune_prev ? collapse4(lbp[k], A.t_prev) : lbp[k];
+          if (m > 0) r[k] = update4(r[k], lp[k], S.dlt);
+          if (wr) gL[w] = prune ? collapse4(lp[k], t) : lp[k];
           out[w] = r[k];
           const double a = r[k].x, b = r[k].y, cc = r[k].z, d = r[k].w;
           ss = __dadd_rn(ss, __dmul_rn(a, a));
@@ -569,91 +817,131 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
         }
       }
       const double v = warp_sum_f64(ss);
-      if (lane == 0) {
-        S.wsum[0][warp] = v;
-        S.wcnt[0][warp] = 0u;
-      }
+      if (lane == 0) S.wsum[warp][0] = v;
+      named_arrive(BAR_PARTIALS, kBarWC);
+      break;
+    }
+    if (tl) tl[(size_t)(e + 1) * 8 + 1] = gtimer();
+    // ---- B_e: tree e+2's refresh + counts, hidden behind the exchange
+    uint32_t lnn[W];
+    const int j2 = e + 2;
+    if (j2 < m) {
+      mbar_wait(&S.mbar[j2 % kRing], (uint32_t)((j2 / kRing) & 1));
+      refresh_count<W>(lnn, G.slot(j2), G, G.hdr[j2], rec_hdr(G.rec(j2)).slot_node, S.wcnt[j2 & 1][warp], tid,
+                       lane);
+      fence_proxy_async();  // generic reads of the ring slot before its next TMA refill
+      named_arrive(BAR_COUNTS, kBarWH);
+    } else {
+#pragma unroll
+      for (int k = 0; k < W; ++k) lnn[k] = 0u;
     }
 #pragma unroll
-    for (int k = 0; k < W; ++k) {  // rotate: e-1 <- e <- e+1
-      lbp[k] = lbc[k];
-      lbc[k] = lbn[k];
+    for (int k = 0; k < W; ++k) {  // rotate: e-1 <- e <- e+1 <- e+2
+      lp[k] = lc[k];
+      lc[k] = ln[k];
+      ln[k] = lnn[k];
     }
-    if (tl && e >= 0) tl[(size_t)e * 8 + 2] = clock64();
-    fence_proxy_async();
-    __syncthreads();                // partials complete
-    named_sync(1, kSweepThreads);   // decision of tree e installed (S.dlt, flags)
-    if (tl && e >= 0) tl[(size_t)e * 8 + 3] = clock64();
+    if (tl) tl[(size_t)(e + 1) * 8 + 2] = gtimer();
+    if (e >= 0) named_sync(BAR_DECISION, kBarWC);  // decision of tree e installed (S.dlt, flags)
+    if (tl) tl[(size_t)(e + 1) * 8 + 3] = gtimer();
   }
 }
 
-// Control warp: TMA/stage streaming, exchange, decision, bookkeeping.
+// Control warp: exchange and decision, nothing else.
 __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
-                                             const DecConst &K, long long *dtl) {
+                                             const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
-  auto issue_tree = [&](int j) {  // lane 0
+  __syncthreads();  // prologue barrier
+  for (int e = 0; e <= m; ++e) {
+    const bool has_cur = e < m;
+    const TreeHdr hd = has_cur ? G.hdr[e] : TreeHdr{};
+    const int ns = has_cur ? hd.nslots : 1;  // e == m: sum of squares in slot 0
+    const int set = (int)((xbase + (unsigned long long)e) % kXSets);
+    const bool fast = ns < 32;
+
+    named_sync(BAR_PARTIALS, kBarWC);  // A_e partials complete
+    if (tl) tl[(size_t)(e + 1) * 8 + 4] = gtimer();
+    if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 0] = nstimer();
+    exchange_add(c, S, ns, set, lane);
+    DecIn I;
+    if (has_cur) {
+      named_sync(BAR_HDONE, kBarCH);  // helper: prep(e) ready, done with dec[e & 1]
+      if (fast) decide_load(I, S.prep[e & 1], G.rec(e), hd, lane);
+    }
+    double tot[kPollSlots];
+    exchange_poll(c, S, ns, set, lane, tot);
+    if (tl) tl[(size_t)(e + 1) * 8 + 5] = gtimer();
+    if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 1] = nstimer();
+    if (has_cur && fast) {
+      decide_fast(S, S.dec[e & 1], I, tot[0], hd, lane, K);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kPollSlots; ++i)
+        if (lane + 32 * i < ns) S.tot_sum[lane + 32 * i] = tot[i];
+      __syncwarp();
+      if (has_cur) {
+        decide(S, S.prep[e & 1], S.dec[e & 1], G.rec(e), hd, lane, K);
+        named_arrive(BAR_DECISION, kBarWC);
+      }
+    }
+    if (tl) tl[(size_t)(e + 1) * 8 + 6] = gtimer();
+    named_arrive(BAR_HREADY, kBarCH);
+  }
+}
+
+// Helper warp: prefetch, count channel, count-only precomputation, bookkeeping.
+__device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
+                                            const DecConst &K, unsigned long long xbase, long long *tl) {
+  const int m = G.m;
+  auto issue_tree = [&](int j) {  // lane 0: cache row, split column, record -> ring slot j % kRing
     const TreeHdr hd = G.hdr[j];
     unsigned long long *mb = &S.mbar[j % kRing];
-    uint8_t *dst = G.ring + (size_t)(j % kRing) * 2 * G.chunk;
+    uint8_t *dst = G.slot(j);
     const bool g = hd.kind == KIND_GROW;
-    fence_proxy_async();
-    mbar_expect(mb, g ? 2u * G.lenp : G.lenp);
+    const uint32_t rb = (uint32_t)c.rstride;
+    mbar_expect(mb, (g ? 2u * G.lenp : G.lenp) + rb);
     bulk_g2s(dst, c.L + (size_t)j * c.n_pad + G.start, G.lenp, mb);
     if (g) bulk_g2s(dst + G.chunk, c.Xt + (size_t)hd.axis * c.n_pad + G.start, G.lenp, mb);
+    bulk_g2s(dst + 2 * (size_t)G.chunk, c.rec + (size_t)j * rb, rb, mb);
   };
-  // baseline of the monotonic accumulators: CTA 0 saved their values at the
-  // end of the previous sweep (the live words may already be moving)
-  for (int i = lane; i < (kSlotsMax + 1) * 5; i += 32) S.prev[i / 5][i % 5] = c.accum_base[i];
-  unsigned long long counter = c.accum_base[(kSlotsMax + 1) * 5];
-  for (int j = 0; j < 2 && j < m; ++j) {
-    if (lane == 0) issue_tree(j);
-    stage_load(c, S.stage[j], j, lane);
-  }
-  cp_async_wait_all();
+  auto prepare_tree = [&](int j) {
+    mbar_wait(&S.mbar[j % kRing], (uint32_t)((j / kRing) & 1));
+    counts_poll(c, S, j, G.hdr[j].nslots, lane);
+    prepare(S.prep[j & 1], S.hcnt, G.rec(j), G.size, G.hdr[j], lane, K);
+    named_arrive(BAR_HDONE, kBarCH);
+  };
+  if (lane == 0)
+    for (int j = 0; j < kRing && j < m; ++j) issue_tree(j);
   __syncthreads();  // prologue barrier
-
-  for (int e = -1; e <= m; ++e) {
-    const bool has_cur = e >= 0 && e < m, has_next = e + 1 < m;
-    const TreeHdr hc = has_cur ? G.hdr[e] : TreeHdr{};
-    const TreeHdr hn = has_next ? G.hdr[e + 1] : TreeHdr{};
-    const int nsx = e == m ? 1 : (hc.nslots > hn.nslots ? hc.nslots : hn.nslots);
-    // two trees ahead: ring slot / stage (e+2)%3 held tree e-1, whose last
-    // users (pass e-2, decide_post(e-1)) are done
-    if (e >= 0 && e + 2 < m) {
-      if (lane == 0) issue_tree(e + 2);
-      stage_load(c, S.stage[(e + 2) % kRing], e + 2, lane);
+  for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
+    named_sync(BAR_COUNTS, kBarWH);
+    counts_add(c, S, j, G.hdr[j].nslots, lane);
+  }
+  if (m > 0) prepare_tree(0);
+  for (int e = 0; e <= m; ++e) {
+    if (e + 2 < m) {  // B_e done: publish the counts of tree e+2
+      named_sync(BAR_COUNTS, kBarWH);
+      counts_add(c, S, e + 2, G.hdr[e + 2].nslots, lane);
     }
-    __syncthreads();  // worker partials complete
-    if (dtl && e >= 0) dtl[(size_t)e * 8 + 0] = clock64();
-    counter += (unsigned long long)G.nblk;
-    exchange(c, S, nsx, counter, lane);
-    if (dtl && e >= 0) dtl[(size_t)e * 8 + 1] = clock64();
-    if (has_cur) decide(S, S.prep[e & 1], S.stage[e % kRing], hc, lane, K);
-    if (dtl && e >= 0) dtl[(size_t)e * 8 + 2] = clock64();
-    if (e + 1 < m) cp_async_wait_all();  // stage e+2 before pass e+1 reads its leaf list
-    named_arrive(1, kSweepThreads);       // workers may start the next pass
-    if (has_next) prepare(S, S.prep[(e + 1) & 1], S.stage[(e + 1) % kRing], hn, lane, K);
-    if (G.cta == 0) {
-      if (has_cur) decide_post(c, S, S.prep[e & 1], S.stage[e % kRing], hc, e, lane, K);
-      if (e == m && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
-        const HP &hp = c.hp;
-        const double s2 = __ddiv_rn(__dadd_rn(__dmul_rn(hp.nu, hp.lam), S.tot_sum[0]), *c.rand_chi2);
-        *c.sigma2_draw = s2;
-        if (hp.update_sigma) *c.sigma2 = s2;
-        *c.iter_dev += 1ull;
-      }
-      if (e == m) {  // baseline for the next sweep: every accumulator's final value
-        __syncwarp();
-        for (int i = lane; i < (kSlotsMax + 1) * 5; i += 32) c.accum_base[i] = S.prev[i / 5][i % 5];
-        if (lane == 0) c.accum_base[(kSlotsMax + 1) * 5] = counter;
-      }
+    named_sync(BAR_HREADY, kBarCH);  // exchange e done, decision e taken
+    if (e + 1 < m) prepare_tree(e + 1);
+    if (tl) tl[(size_t)(e + 1) * 8 + 7] = gtimer();
+    if (e < m && G.cta == e % G.nblk) decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K);
+    if (e == m && G.cta == m % G.nblk && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
+      const HP &hp = c.hp;
+      const double s2 = __ddiv_rn(__dadd_rn(__dmul_rn(hp.nu, hp.lam), S.tot_sum[0]), *c.rand_chi2);
+      *c.sigma2_draw = s2;
+      if (hp.update_sigma) *c.sigma2 = s2;
+      *c.iter_dev += 1ull;
     }
-    if (dtl && e >= 0) dtl[(size_t)e * 8 + 3] = clock64();
-    if (c.trace && lane == 0 && e >= 0) {
-      unsigned long long g;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-      c.trace[((size_t)e * G.nblk + G.cta) * 2 + 1] = (long long)g;
+    if (e == m && G.cta == 0) {  // the next sweep's exchange baselines
+      if (lane == 0) c.xsnap[0] = xbase + (unsigned long long)(m + 1);
+      const unsigned long long *src = &S.xprev[0][0][0];
+      for (int i = lane; i < kXSets * (kSlotsMax + 1) * 3; i += 32) c.xsnap[1 + i] = src[i];
+      const unsigned long long *cs = &S.cprev[0][0];
+      for (int i = lane; i < kCSets * (int)kCSetWords; i += 32) c.csnap[i] = cs[i];
     }
+    if (e < m && e + kRing < m && lane == 0) issue_tree(e + kRing);  // slot of tree e is free
   }
 }
 
@@ -664,9 +952,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   Geom G;
   G.m = c.m;
   G.chunk = c.chunk;
+  G.size = c.size;
   G.hdr = reinterpret_cast<TreeHdr *>(smem_raw + sizeof(SweepSmem));
-  // ring slot q: leaf-index row at ring + q*2*chunk, split column right after it
   G.ring = smem_raw + sizeof(SweepSmem) + ((((size_t)c.m * sizeof(TreeHdr)) + 15) & ~(size_t)15);
+  G.slot_bytes = (uint32_t)ring_slot_bytes(c.chunk, c.rstride);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   G.cta = blockIdx.x;
   G.nblk = gridDim.x;
@@ -676,26 +965,37 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   G.nwords = (int)(G.lenp >> 2);
 
   for (int i = tid; i < c.m; i += kSweepThreads) G.hdr[i] = c.hdr[i];
+  {  // exchange baselines: the words' values when the previous sweep ended
+    unsigned long long *dst = &S.xprev[0][0][0];
+    for (int i = tid; i < kXSets * (kSlotsMax + 1) * 3; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
+    unsigned long long *cd = &S.cprev[0][0];
+    for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cd[i] = c.csnap[i];
+  }
   if (tid == 0) {
     for (int q = 0; q < kRing; ++q) mbar_init(&S.mbar[q]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    S.flag_wr = 0;
+    S.flag_prune = 0;
+    S.flag_t = 0;
   }
   for (int h = tid; h < 256; h += kSweepThreads) S.dlt[h] = 0.f;  // index 0 = padding points
+  const unsigned long long xbase = c.xsnap[0];
   __syncthreads();
 
-  if (warp == kWorkWarps) {
+  if (warp >= kCtrlWarp) {
     DecConst K;
     const double sigma2 = *c.sigma2;  // the sweep uses the old sigma2 (sampler.py:906)
     K.tau = __ddiv_rn(1.0, sigma2);
     K.tau_mu = __ddiv_rn(1.0, __dmul_rn(c.hp.leaf_sd, c.hp.leaf_sd));
     K.prior = __dmul_rn(K.tau_mu, c.hp.leaf_mean);
     K.lm_term = __dmul_rn(__dmul_rn(__dmul_rn(0.5, c.hp.leaf_mean), c.hp.leaf_mean), K.tau_mu);
-    long long *dtl = (c.timeline && G.cta == 0 && lane == 0) ? c.timeline + (size_t)2 * (c.m + 1) * 8 : nullptr;
-    control_loop(c, S, G, lane, K, dtl);
+    long long *tl = (c.timeline && G.cta == 0 && lane == 0) ? c.timeline : nullptr;
+    if (warp == kCtrlWarp)
+      control_loop(c, S, G, lane, K, xbase, tl);
+    else
+      helper_loop(c, S, G, lane, K, xbase, tl);
   } else {
-    long long *tl = nullptr;
-    if (c.timeline && tid == 0 && (G.cta == 0 || G.cta == G.nblk - 1))
-      tl = c.timeline + (size_t)(G.cta == 0 ? 0 : 1) * (c.m + 1) * 8;
+    long long *tl = (c.timeline && tid == 0 && G.cta == 0) ? c.timeline : nullptr;
     worker_loop<W>(c, S, G, tid, warp, lane, tl);
   }
 }
@@ -706,8 +1006,7 @@ static SweepFn sweep_fn(int W) {
     case 1: return sweep_kernel<1>;
     case 2: return sweep_kernel<2>;
     case 4: return sweep_kernel<4>;
-    case 8: return sweep_kernel<8>;
-    default: return sweep_kernel<16>;
+    default: return sweep_kernel<8>;
   }
 }
 
@@ -729,7 +1028,7 @@ cudaError_t sweep_prepare(size_t smem) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  for (int W : {1, 2, 4, 8, 16}) {
+  for (int W : {1, 2, 4, 8}) {
     cudaError_t e = cudaFuncSetAttribute(sweep_fn(W), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          optin > (int)smem ? optin : (int)smem);
     if (e != cudaSuccess) return e;

@@ -1,8 +1,10 @@
-"""Per-phase breakdown of the sweep kernel from on-device clock64 stamps.
+"""Per-phase breakdown of the sweep kernel from on-device clock64 stamps (CTA 0, cycles).
 
 usage: python tools/timeline.py [n] [p] [m]
+Worker thread 0: A start, A published, B done, decision received.
+Control lane 0: partials synced, exchange complete, decision published; helper: next tree prepared.
 """
-import sys, os, time
+import sys, os
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2410_23244_b200 import _build, _native as N
@@ -22,27 +24,28 @@ run(st, hp, 20); st.sync()
 N.check(N.lib().bart_set_timeline(st.handle, 1))
 ms = np.zeros(3, np.float32)
 N.check(N.lib().bart_profile(st.handle, 3, N.ptr(ms)))
-tl = np.zeros((3, m + 1, 8), np.int64)
+tl = np.zeros((3, m + 2, 8), np.int64)
 N.check(N.lib().bart_get_timeline(st.handle, N.ptr(tl)))
-print(f"n={n} p={p} m={m} sweep {ms[1]/3:.3f} ms/launch, {ms[1]/3/m*1e3:.2f} us/tree; cfg {st.sweep_config()}")
-names = ["wait_data", "pass", "sync+exchange+decide"]
-for c, lab in ((0, "CTA0"), (1, "CTAlast")):
-    t = tl[c]
-    d = np.diff(t[:m, :4], axis=1)          # phases within tree
-    nxt = t[1:m + 1, 0] - t[:m, 3]           # end -> next start
-    med = np.median(d, axis=0)
-    print(lab, " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, med)), f"loop={np.median(nxt):.0f}",
-          f"total/tree={np.median(t[1:m+1,0]-t[:m,0]):.0f} cyc")
-    print("   p90:", " ".join(f"{nm}={v:.0f}" for nm, v in zip(names, np.percentile(d, 90, axis=0))))
-dd = np.diff(tl[2, :m, :4], axis=1)
-print("control warp CTA0 (cyc):", *[f"{v:.0f}" for v in np.median(dd, axis=0)], "[exchange, decide, prepare+post]")
+print(f"n={n} p={p} m={m} sweep {ms[1]/3:.3f} ms/launch, {ms[1]/3/m*1e3:.2f} us/tree, propose {ms[2]/3*1e3:.1f} us; cfg {st.sweep_config()}")
+t = tl[0][1:m + 1].astype(float)  # rows for trees 0..m-1
+q = lambda a: f"{np.median(a):6.0f} (p90 {np.percentile(a, 90):6.0f})"
+print("worker  A pass          ", q(t[:, 1] - t[:, 0]))
+print("worker  B pass          ", q(t[:, 2] - t[:, 1]))
+print("worker  wait decision   ", q(t[:, 3] - t[:, 2]))
+print("control publish->synced ", q(t[:, 4] - t[:, 1]))
+print("control exchange        ", q(t[:, 5] - t[:, 4]))
+print("control decide          ", q(t[:, 6] - t[:, 5]))
+print("helper prepare done     ", q(t[:, 7] - t[:, 6]))
+print("decision -> worker      ", q(t[:, 3] - t[:, 6]))
+print("tree period (cycles)    ", q(np.diff(tl[0][1:m + 2, 0].astype(float))))
 nb = st.sweep_config()["ctas"]
-tr = np.zeros((m + 1, nb, 2), np.int64)
+tr = np.zeros((m + 2, nb, 2), np.int64)
 N.check(N.lib().bart_get_trace(st.handle, N.ptr(tr)))
-done = tr[:m, :, 1].astype(float)
-spread = done.max(1) - done.min(1)
-period = np.diff(done.max(1))
-q = lambda a: f"median {np.median(a):.0f} p90 {np.percentile(a, 90):.0f} ns"
-print("control-done spread over CTAs:", q(spread))
-print("tree period:", q(period))
+pub = tr[1:m + 1, :, 0].astype(float)
+done = tr[1:m + 1, :, 1].astype(float)
+print("arrival skew (ns): last publish - first publish ", q(pub.max(1) - pub.min(1)))
+print("detection jitter (ns): last done - first done  ", q(done.max(1) - done.min(1)))
+print("exchange latency (ns): first done - last publish", q(done.min(1) - pub.max(1)))
+late = np.argmax(pub, axis=1)
+print("latest publisher CTA histogram (top 5):", np.bincount(late, minlength=nb).argsort()[::-1][:5])
 st.close()
