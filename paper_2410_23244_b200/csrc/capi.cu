@@ -236,7 +236,7 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   OWN(s2d, 1);
   OWN(acc, (size_t)c.m);
   OWN(xacc, (size_t)kXSets * kXSetWords);
-  OWN(xsnap, 1 + (size_t)kXSets * (kSlotsMax + 1) * 4);
+  OWN(xsnap, 1 + (size_t)kXSets * kXSetWords);
   OWN(errf, 32);
   OWN(cacc, (size_t)kCSets * kCSetWords);
   OWN(csnap, (size_t)kCSets * kCSetWords);

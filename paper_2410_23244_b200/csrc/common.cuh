@@ -26,11 +26,13 @@ constexpr int kMaxCtas = 256;         // CTAs per shard (one per SM)
 constexpr int kProposeWarps = 4;
 constexpr int kMaxShards = 8;         // n-shards whose exchange words a sweep adds into
 // Exchange accumulators: kXSets sets (exchange X uses set X % kXSets), each
-// kSlotsMax+1 slot lines of kXLineWords u64 (128 B): 3 fixed-point limbs of
-// the slot's f64 residual sum, 1 point count, padding.
+// kSlotsMax+1 slot sectors of kXSlotWords u64 (32 B): 3 fixed-point limbs of
+// the slot's f64 residual sum + one unused word.  One warp instruction adds
+// (and polls) 8 slots: lane 4s+q owns word q of slot s, so the L2 sees one
+// coalesced 32-B atomic per slot per CTA.
 constexpr int kXSets = 3;
-constexpr int kXLineWords = 16;
-constexpr size_t kXSetWords = (size_t)(kSlotsMax + 1) * kXLineWords;
+constexpr int kXSlotWords = 4;
+constexpr size_t kXSetWords = (size_t)(kSlotsMax + 1) * kXSlotWords;
 // Count channel: the per-leaf point counts of tree j (needed one exchange
 // before tree j's decision) travel through their own tagged words, set j % 4,
 // one u64 per slot, added and polled by the helper warps.

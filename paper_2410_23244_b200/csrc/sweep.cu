@@ -50,14 +50,16 @@ constexpr unsigned long long kTagOne = 1ull << kTagShift;
 constexpr unsigned long long kDataMask = kTagOne - 1ull;
 constexpr int kLimbBits = 37;
 constexpr unsigned long long kLimbMask = (1ull << kLimbBits) - 1ull;
-constexpr int kPollSlots = (kSlotsMax + 1 + 31) / 32;  // slots per control lane
+constexpr int kFastRounds = 4;  // exchange rounds (8 slots each) kept in registers: trees with <= 32 slots
 constexpr int kCtrlWarp = kWorkWarps;  // then the helper warp
 
-// named barriers (0 is __syncthreads) and their thread counts
-enum : int { BAR_PARTIALS = 1, BAR_DECISION = 2, BAR_HREADY = 3, BAR_HDONE = 4, BAR_COUNTS = 5 };
-constexpr int kBarWC = kWorkers + 32;  // workers + control (PARTIALS, DECISION)
-constexpr int kBarWH = kWorkers + 32;  // workers + helper (COUNTS)
-constexpr int kBarCH = 64;             // control + helper (HREADY, HDONE)
+// Named barriers (0 is __syncthreads) only where the two sides strictly
+// alternate: workers publish A_e (PARTIALS) and then wait for decision e
+// (DECISION).  Signals whose producer may run a tree ahead of its consumer
+// (counts -> helper, prep -> control, decision -> helper) are mbarriers with
+// one phase per tree and a buffer per tree parity.
+enum : int { BAR_PARTIALS = 1, BAR_DECISION = 2 };
+constexpr int kBarWC = kWorkers + 32;  // workers + control
 
 // count-only precomputation for one tree (see prepare())
 struct Prep {
@@ -65,7 +67,8 @@ struct Prep {
   double prec[kSlotsMax];  // tau_mu + n * tau
   double zs[kSlotsMax];    // z / sqrt(prec)
   double cadj[kSlotsMax];  // n * adj, the tree's own contribution to the sums
-  double prec_l, prec_r, prec_p, zs_p, partial;
+  double rcp[kSlotsMax];   // 1 / prec, correctly rounded (division by Markstein's correction)
+  double prec_l, prec_r, prec_p, zs_p, partial, rcp_p;
 };
 
 // decision outputs of one tree, read by the helper's bookkeeping
@@ -85,9 +88,12 @@ struct __align__(16) SweepSmem {
   double q_s[kSlotsMax + 1];                // posterior means (control scratch, wide trees)
   float row[256];                           // new leaf row (helper scratch)
   float dlt[256];                           // residual delta by larger-tree heap index
-  unsigned long long xprev[kXSets][kSlotsMax + 1][3];  // last complete value of every exchange word
+  unsigned long long xprev[kXSets][kXSetWords];       // last complete value of every exchange word
   unsigned long long cprev[kCSets][kCSetWords];       // last complete value of every count word
-  unsigned long long mbar[kRing];
+  unsigned long long mbar[kRing];      // TMA ring slot filled (per tree j % kRing)
+  unsigned long long cnt_mbar[2];     // workers -> helper: B pass counts of tree t in wcnt[t & 1]
+  unsigned long long prep_mbar[2];    // helper -> control: prep[t & 1] ready
+  unsigned long long dec_mbar[2];     // control -> helper: decision t in dec[t & 1] (t = m: sum r^2)
   int flag_wr, flag_prune, flag_t;
 };
 
@@ -109,9 +115,14 @@ int sweep_words_per_thread(int chunk) {
 
 // ------------------------------------------------------------ async copies, barriers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long *b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count = 1) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// phase of tree t on a per-parity mbarrier
+__device__ __forceinline__ uint32_t par2(int t) { return (uint32_t)((t >> 1) & 1); }
 __device__ __forceinline__ void mbar_expect(unsigned long long *b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
@@ -369,27 +380,33 @@ __device__ __forceinline__ void ld_poll2(const unsigned long long *p, unsigned l
 
 // Control warp, exchange X: fold the worker warps' f64 partials of ns slots
 // (fixed order), add them as fixed-point limbs into every shard's copy of set
-// X % 3.  exchange_poll then waits until every word of the local copy carries
-// one more arrival per CTA than its last complete value; lane s returns the
-// total of slot s (and s + 32, ... in tot[]).
+// X % 3.  Lane 4j+q handles word q of slot 8k+j, so each warp instruction
+// carries 8 slots and the L2 sees one coalesced atomic per slot per CTA (the
+// four lanes of a slot fold it redundantly).
+__device__ __forceinline__ unsigned long long pick3(const unsigned long long (&l)[3], int q) {
+  return q == 0 ? l[0] : (q == 1 ? l[1] : l[2]);
+}
+
 __device__ __forceinline__ void exchange_add(const ChainDev &c, const SweepSmem &S, int ns, int set, int lane) {
   const bool sys = c.shard_sys != 0;
   const size_t set_off = (size_t)set * kXSetWords;
-  for (int s = lane; s < ns; s += 32) {
-    double w[kWorkWarps];
+  const int q = lane & 3;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    const int s = s0 + (lane >> 2);
+    if (s < ns) {
+      double w[kWorkWarps];
 #pragma unroll
-    for (int k = 0; k < kWorkWarps; ++k) w[k] = S.wsum[k][s];
+      for (int k = 0; k < kWorkWarps; ++k) w[k] = S.wsum[k][s];
 #pragma unroll
-    for (int step = 1; step < kWorkWarps; step <<= 1)  // fixed pairwise order
+      for (int step = 1; step < kWorkWarps; step <<= 1)  // fixed pairwise order
 #pragma unroll
-      for (int k = 0; k + step < kWorkWarps; k += 2 * step) w[k] = __dadd_rn(w[k], w[k + step]);
-    unsigned long long l[3];
-    to_limbs(w[0], l, c.err);
-    for (int g = 0; g < c.n_shards; ++g) {
-      unsigned long long *a = c.xpeer[g] + set_off + (size_t)s * kXLineWords;
-      red_add(a + 0, kTagOne | l[0], sys);
-      red_add(a + 1, kTagOne | l[1], sys);
-      red_add(a + 2, kTagOne | l[2], sys);
+        for (int k = 0; k + step < kWorkWarps; k += 2 * step) w[k] = __dadd_rn(w[k], w[k + step]);
+      unsigned long long l[3];
+      to_limbs(w[0], l, c.err);
+      if (q < 3) {
+        const unsigned long long v = kTagOne | pick3(l, q);
+        for (int g = 0; g < c.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, v, sys);
+      }
     }
   }
 }
@@ -401,47 +418,78 @@ __device__ __forceinline__ void ld_poll1s(const unsigned long long *p, unsigned 
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");
 }
 
-__device__ __forceinline__ void exchange_poll(const ChainDev &c, SweepSmem &S, int ns, int set, int lane,
-                                              double (&tot)[kPollSlots]) {
+// Poll rounds [k0, k0+R) of set `set` until every used word is complete; on
+// return lane 4j (q == 0) holds in tot[k] the total of slot 8(k0+k)+j.
+template <int R>
+__device__ __forceinline__ void poll_rounds(const ChainDev &c, SweepSmem &S, int ns, int set, int k0, int lane,
+                                            double (&tot)[R]) {
   const bool sys = c.shard_sys != 0;
   const unsigned long long target = (unsigned long long)c.nblk_total << kTagShift;
   const unsigned long long *base = c.xacc + (size_t)set * kXSetWords;
-  unsigned long long w[kPollSlots][3];
+  unsigned long long *prev = S.xprev[set];
+  const int q = lane & 3;
+  unsigned long long w[R];
   bool done;
   do {
     bool ok = true;
 #pragma unroll
-    for (int i = 0; i < kPollSlots; ++i) {
-      const int s = lane + 32 * i;
-      if (s < ns) {
-        const unsigned long long *a = base + (size_t)s * kXLineWords;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          if (sys)
-            ld_poll1s(a + k, w[i][k]);
-          else
-            ld_poll1(a + k, w[i][k]);
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) ok = ok && ((w[i][k] - S.xprev[set][s][k]) & ~kDataMask) == target;
+    for (int k = 0; k < R; ++k) {
+      const int s = 8 * (k0 + k) + (lane >> 2);
+      w[k] = 0ull;
+      if (s < ns && q < 3) {
+        const size_t i = (size_t)s * kXSlotWords + q;
+        if (sys)
+          ld_poll1s(base + i, w[k]);
+        else
+          ld_poll1(base + i, w[k]);
+        ok = ok && ((w[k] - prev[i]) & ~kDataMask) == target;
       }
     }
     done = __all_sync(0xffffffffu, ok);
   } while (!done);
 #pragma unroll
-  for (int i = 0; i < kPollSlots; ++i) {
-    const int s = lane + 32 * i;
-    tot[i] = 0.0;
-    if (s < ns) {
-      unsigned long long d[3];
+  for (int k = 0; k < R; ++k) {
+    const int s = 8 * (k0 + k) + (lane >> 2);
+    unsigned long long d = 0ull;
+    if (s < ns && q < 3) {
+      const size_t i = (size_t)s * kXSlotWords + q;
+      d = (w[k] - prev[i]) & kDataMask;
+      prev[i] = w[k];
+    }
+    const unsigned long long d1 = __shfl_down_sync(0xffffffffu, d, 1), d2 = __shfl_down_sync(0xffffffffu, d, 2);
+    tot[k] = from_limbs(d, d1, d2);
+  }
+}
+
+// Trees with <= 32 slots: returns the total of slot `lane` in every lane.
+__device__ __forceinline__ double exchange_poll_fast(const ChainDev &c, SweepSmem &S, int ns, int set, int lane) {
+  const int rounds = (ns + 7) >> 3;
+  double mine = 0.0;
+  if (rounds <= 1) {
+    double t[1];
+    poll_rounds<1>(c, S, ns, set, 0, lane, t);
+    mine = __shfl_sync(0xffffffffu, t[0], (lane & 7) * 4);
+  } else {
+    double t[kFastRounds];
+    poll_rounds<kFastRounds>(c, S, ns, set, 0, lane, t);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        d[k] = (w[i][k] - S.xprev[set][s][k]) & kDataMask;
-        S.xprev[set][s][k] = w[i][k];
-      }
-      tot[i] = from_limbs(d[0], d[1], d[2]);
+    for (int k = 0; k < kFastRounds; ++k) {
+      const double v = __shfl_sync(0xffffffffu, t[k], (lane & 7) * 4);
+      if ((lane >> 3) == k) mine = v;
     }
   }
+  return mine;
+}
+
+// Any number of slots, one round (8 slots) at a time: totals into S.tot_sum.
+__device__ __forceinline__ void exchange_poll_slow(const ChainDev &c, SweepSmem &S, int ns, int set, int lane) {
+  for (int k0 = 0; 8 * k0 < ns; ++k0) {
+    double t[1];
+    poll_rounds<1>(c, S, ns, set, k0, lane, t);
+    const int s = 8 * k0 + (lane >> 2);
+    if ((lane & 3) == 0 && s < ns) S.tot_sum[s] = t[0];
+  }
+  __syncwarp();
 }
 
 // Helper warp, count channel: add this CTA's per-leaf counts of tree j into
@@ -492,6 +540,17 @@ struct DecConst {
 
 __device__ __forceinline__ bool is_child(int h, int t, bool move) { return move && h >= 2 && (h >> 1) == t; }
 
+// a / b for b > 0 given y = RN(1/b): q0 = RN(a*y) is faithful, the residual
+// a - b*q0 is exact in one FMA, and RN(q0 + r*y) is the correctly rounded
+// quotient (Markstein).  Bit-identical to __ddiv_rn on 5e9 samples of the
+// decision's operand ranges (tools/divtest.cu), at a third of its latency.
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = __fma_rn(-b, q0, a);
+  const double q1 = __fma_rn(r, y, q0);
+  return a == 0.0 ? a : q1;
+}
+
 // Helper warp: count-only terms of tree j, from the counts the previous
 // exchange delivered.  Same operations, in the same order, as the reference:
 // prec = tau_mu + n*tau, z/sqrt(prec) (sampler.py:579-595), adjustment n*adj
@@ -511,6 +570,7 @@ __device__ __forceinline__ void prepare(Prep &P, const uint32_t *tot_cnt, const 
     P.cnt[j] = cn;
     P.cadj[j] = __dmul_rn((double)cn, (double)a32);
     P.prec[j] = prec;
+    P.rcp[j] = __drcp_rn(prec);
     P.zs[j] = __ddiv_rn(z[h], __dsqrt_rn(prec));
   }
   __syncwarp();
@@ -522,6 +582,7 @@ __device__ __forceinline__ void prepare(Prep &P, const uint32_t *tot_cnt, const 
       P.prec_l = prec_l;
       P.prec_r = prec_r;
       P.prec_p = prec_p;
+      P.rcp_p = __drcp_rn(prec_p);
       P.zs_p = __ddiv_rn(z[t], __dsqrt_rn(prec_p));
     } else {
       const double q = __ddiv_rn(__dmul_rn(K.tau_mu, prec_p), __dmul_rn(prec_l, prec_r));
@@ -543,21 +604,23 @@ __device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, Dec &Do, con
   const int sl_i = hd.slot_l, sr_i = hd.slot_r;
   for (int base = 0; base <= ns; base += 32) {
     const int j = base + lane;
-    double num = 1.0, den = 1.0, zs = 0.0;
+    double num = 1.0, den = 1.0, rcp = 1.0, zs = 0.0;
     if (j < ns) {
       const double sums = __dadd_rn(S.tot_sum[j], P.cadj[j]);  // sampler.py:570-576
       Do.sums_s[j] = sums;
       num = __dadd_rn(K.prior, __dmul_rn(K.tau, sums));
       den = P.prec[j];
+      rcp = P.rcp[j];
       zs = P.zs[j];
     } else if (j == ns && move) {  // the collapsed parent: count nl+nr, sum sl+sr (sampler.py:861-866)
       const double sl = __dadd_rn(S.tot_sum[sl_i], P.cadj[sl_i]);
       const double sr = __dadd_rn(S.tot_sum[sr_i], P.cadj[sr_i]);
       num = __dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr)));
       den = P.prec_p;
+      rcp = P.rcp_p;
       zs = P.zs_p;
     }
-    const double q = __ddiv_rn(num, den);
+    const double q = div_rcp(num, den, rcp);
     if (j <= ns) {
       S.q_s[j] = q;
       Do.v_s[j] = __dadd_rn(q, zs);
@@ -611,7 +674,7 @@ __device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, Dec &Do, con
 // loaded before the exchange completes, so after the poll the critical path
 // is one division, three shuffles and the ratio.
 struct DecIn {
-  double cadj, den, zs, cadj_l, cadj_r;
+  double cadj, den, rcp, zs, cadj_l, cadj_r;
   float oldv;
   int h;
   bool child;
@@ -626,6 +689,7 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
   I.cadj = 0.0;
   I.den = 1.0;
+  I.rcp = 1.0;
   I.zs = 0.0;
   I.cadj_l = I.cadj_r = 0.0;
   I.oldv = 0.f;
@@ -634,6 +698,7 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
   if (lane < ns) {
     I.cadj = P.cadj[lane];
     I.den = P.prec[lane];
+    I.rcp = P.rcp[lane];
     I.zs = P.zs[lane];
     I.h = mv.slot_node[lane];
     I.child = is_child(I.h, t, move);
@@ -642,6 +707,7 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
     I.cadj_l = P.cadj[hd.slot_l];
     I.cadj_r = P.cadj[hd.slot_r];
     I.den = P.prec_p;
+    I.rcp = P.rcp_p;
     I.zs = P.zs_p;
   }
   if (lane == 0) {
@@ -668,7 +734,7 @@ __device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &
     const double sl = __dadd_rn(tl, I.cadj_l), sr = __dadd_rn(tr, I.cadj_r);
     num = __dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr)));
   }
-  const double q = __ddiv_rn(num, I.den);
+  const double q = div_rcp(num, I.den, I.rcp);
   const double v = __dadd_rn(q, I.zs);
   const double ml = __shfl_sync(0xffffffffu, q, sl_i), mr = __shfl_sync(0xffffffffu, q, sr_i);
   const double mp = __shfl_sync(0xffffffffu, q, ns), vp = __shfl_sync(0xffffffffu, v, ns);
@@ -780,7 +846,8 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
   if (m > 0) {  // tree 0: refresh + counts
     mbar_wait(&S.mbar[0], 0u);
     refresh_count<W>(ln, G.slot(0), G, G.hdr[0], rec_hdr(G.rec(0)).slot_node, S.wcnt[0][warp], tid, lane);
-    named_arrive(BAR_COUNTS, kBarWH);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.cnt_mbar[0]);
   }
   for (int e = -1; e <= m; ++e) {
     if (tl) tl[(size_t)(e + 1) * 8 + 0] = gtimer();
@@ -830,7 +897,8 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       refresh_count<W>(lnn, G.slot(j2), G, G.hdr[j2], rec_hdr(G.rec(j2)).slot_node, S.wcnt[j2 & 1][warp], tid,
                        lane);
       fence_proxy_async();  // generic reads of the ring slot before its next TMA refill
-      named_arrive(BAR_COUNTS, kBarWH);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.cnt_mbar[j2 & 1]);
     } else {
 #pragma unroll
       for (int k = 0; k < W; ++k) lnn[k] = 0u;
@@ -865,19 +933,20 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
     exchange_add(c, S, ns, set, lane);
     DecIn I;
     if (has_cur) {
-      named_sync(BAR_HDONE, kBarCH);  // helper: prep(e) ready, done with dec[e & 1]
+      mbar_wait(&S.prep_mbar[e & 1], par2(e));  // helper: prep(e) ready
       if (fast) decide_load(I, S.prep[e & 1], G.rec(e), hd, lane);
     }
-    double tot[kPollSlots];
-    exchange_poll(c, S, ns, set, lane, tot);
+    double tot = 0.0;
+    if (fast)
+      tot = exchange_poll_fast(c, S, ns, set, lane);
+    else
+      exchange_poll_slow(c, S, ns, set, lane);
     if (tl) tl[(size_t)(e + 1) * 8 + 5] = gtimer();
     if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 1] = nstimer();
     if (has_cur && fast) {
-      decide_fast(S, S.dec[e & 1], I, tot[0], hd, lane, K);
+      decide_fast(S, S.dec[e & 1], I, tot, hd, lane, K);
     } else {
-#pragma unroll
-      for (int i = 0; i < kPollSlots; ++i)
-        if (lane + 32 * i < ns) S.tot_sum[lane + 32 * i] = tot[i];
+      if (fast && lane < ns) S.tot_sum[lane] = tot;
       __syncwarp();
       if (has_cur) {
         decide(S, S.prep[e & 1], S.dec[e & 1], G.rec(e), hd, lane, K);
@@ -885,7 +954,8 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
       }
     }
     if (tl) tl[(size_t)(e + 1) * 8 + 6] = gtimer();
-    named_arrive(BAR_HREADY, kBarCH);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.dec_mbar[e & 1]);  // dec[e & 1] (or sum r^2) for the helper
   }
 }
 
@@ -908,24 +978,27 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     mbar_wait(&S.mbar[j % kRing], (uint32_t)((j / kRing) & 1));
     counts_poll(c, S, j, G.hdr[j].nslots, lane);
     prepare(S.prep[j & 1], S.hcnt, G.rec(j), G.size, G.hdr[j], lane, K);
-    named_arrive(BAR_HDONE, kBarCH);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.prep_mbar[j & 1]);
   };
   if (lane == 0)
     for (int j = 0; j < kRing && j < m; ++j) issue_tree(j);
   __syncthreads();  // prologue barrier
   for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
-    named_sync(BAR_COUNTS, kBarWH);
+    mbar_wait(&S.cnt_mbar[j & 1], par2(j));
     counts_add(c, S, j, G.hdr[j].nslots, lane);
   }
   if (m > 0) prepare_tree(0);
   for (int e = 0; e <= m; ++e) {
     if (e + 2 < m) {  // B_e done: publish the counts of tree e+2
-      named_sync(BAR_COUNTS, kBarWH);
+      mbar_wait(&S.cnt_mbar[e & 1], par2(e + 2));
       counts_add(c, S, e + 2, G.hdr[e + 2].nslots, lane);
     }
-    named_sync(BAR_HREADY, kBarCH);  // exchange e done, decision e taken
+    // tree e+1's count-only terms: prep[(e+1)&1] was last read by decide(e-1)
+    // and decide_post(e-1), both done
     if (e + 1 < m) prepare_tree(e + 1);
     if (tl) tl[(size_t)(e + 1) * 8 + 7] = gtimer();
+    mbar_wait(&S.dec_mbar[e & 1], par2(e));  // exchange e done, decision e taken
     if (e < m && G.cta == e % G.nblk) decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K);
     if (e == m && G.cta == m % G.nblk && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
       const HP &hp = c.hp;
@@ -936,8 +1009,8 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     }
     if (e == m && G.cta == 0) {  // the next sweep's exchange baselines
       if (lane == 0) c.xsnap[0] = xbase + (unsigned long long)(m + 1);
-      const unsigned long long *src = &S.xprev[0][0][0];
-      for (int i = lane; i < kXSets * (kSlotsMax + 1) * 3; i += 32) c.xsnap[1 + i] = src[i];
+      const unsigned long long *src = &S.xprev[0][0];
+      for (int i = lane; i < kXSets * (int)kXSetWords; i += 32) c.xsnap[1 + i] = src[i];
       const unsigned long long *cs = &S.cprev[0][0];
       for (int i = lane; i < kCSets * (int)kCSetWords; i += 32) c.csnap[i] = cs[i];
     }
@@ -966,13 +1039,18 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
 
   for (int i = tid; i < c.m; i += kSweepThreads) G.hdr[i] = c.hdr[i];
   {  // exchange baselines: the words' values when the previous sweep ended
-    unsigned long long *dst = &S.xprev[0][0][0];
-    for (int i = tid; i < kXSets * (kSlotsMax + 1) * 3; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
+    unsigned long long *dst = &S.xprev[0][0];
+    for (int i = tid; i < kXSets * (int)kXSetWords; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
     unsigned long long *cd = &S.cprev[0][0];
     for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cd[i] = c.csnap[i];
   }
   if (tid == 0) {
     for (int q = 0; q < kRing; ++q) mbar_init(&S.mbar[q]);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&S.cnt_mbar[q], kWorkWarps);
+      mbar_init(&S.prep_mbar[q]);
+      mbar_init(&S.dec_mbar[q]);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     S.flag_wr = 0;
     S.flag_prune = 0;
