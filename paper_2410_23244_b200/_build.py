@@ -26,20 +26,23 @@ NVCC_FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "bart_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Compile the library; `out`/`defines` build instrumented or experiment variants elsewhere."""
+    lib = out or LIB
+    if not force and not _stale(lib):
+        return lib
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", lib + ".tmp",
+           *[os.path.join(CSRC, f) for f in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -48,8 +51,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")
     if verbose:
         print(res.stderr, file=sys.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
+
+
+TIMELINE_LIB = os.path.join(PKG, "lib", "libbart_b200_timeline.so")
+
+
+def build_timeline() -> str:
+    """The instrumented variant tools/timeline.py loads (per-phase clock stamps)."""
+    return build(out=TIMELINE_LIB, defines=("BART_TIMELINE=1",))
 
 
 if __name__ == "__main__":

@@ -76,11 +76,15 @@ EXPORTS = sorted(list(_SIGS) + list(_I64) + list(_STR))
 _lib = None
 
 
-def load_library(path: str = LIB) -> C.CDLL:
-    """Load and type the shared library (no device needed)."""
+def load_library(path: str | None = None) -> C.CDLL:
+    """Load and type the shared library (no device needed).
+
+    BART_LIB overrides the in-tree path (A/B experiments between builds).
+    """
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("BART_LIB") or LIB
     if not os.path.exists(path):
         raise RuntimeError(
             f"CUDA library {path} is missing; build it with `python -m paper_2410_23244_b200._build` "

@@ -2,6 +2,7 @@
 // step orchestration (propose kernel + persistent sweep, optionally replayed
 // from a CUDA graph), readback taps and measurement hooks.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -179,6 +180,7 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.size = 1 << c.D;
   c.hp = to_hp(hp);
   c.seed = seed;
+  if (const char *dbg = getenv("BART_DBG")) c.dbg = atoi(dbg);
 
   // sweep geometry: one CTA per SM, contiguous 16-aligned chunks
   int sms = 0, optin = 0;

@@ -118,6 +118,7 @@ struct ChainDev {
   long long *timeline;        // optional per-tree phase stamps (clock64), CTA 0 and last CTA
   long long *trace;           // optional (m+1, nblk, 2) globaltimer: publish, gathered
   HP hp;
+  int dbg;  // experiment switches (BART_DBG env var at create; 0 in production)
 };
 
 // ------------------------------------------------------------ Philox4x32-10

@@ -143,8 +143,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-// timeline stamps: SM clock cycles (all stamps of one CTA share one clock)
+// Timeline stamps (tools/timeline.py builds a BART_TIMELINE=1 variant of the
+// library; production builds carry no instrumentation): SM clock cycles, all
+// stamps of one CTA on one clock.
+#ifndef BART_TIMELINE
+#define BART_TIMELINE 0
+#endif
+#define TL_STAMP(cond) if (BART_TIMELINE && (cond))
 __device__ __forceinline__ long long gtimer() { return clock64(); }
+// a stamp that cannot be taken before `dep` is computed
+// (a predicated trap on the value holds issue until the value is ready)
+__device__ __forceinline__ long long gtimer_after(double dep) {
+  long long t;
+  asm volatile("{\n .reg .pred p;\n setp.eq.f64 p, %1, 0d7E4D3C2B1A098765;\n @p trap;\n mov.u64 %0, %%clock64;\n}"
+               : "=l"(t) : "d"(dep) : "memory");
+  return t;
+}
 // cross-CTA trace stamps: the global nanosecond timer
 __device__ __forceinline__ long long nstimer() {
   unsigned long long g;
@@ -188,6 +202,21 @@ __device__ __forceinline__ float4 update4(float4 r, uint32_t l, const float *dlt
   return r;
 }
 
+// acc += v iff h == slot, exactly: fma(v, 1, acc) = RN(acc + v) and
+// fma(v, 0, acc) = acc.  Compare + select of the multiplier's high word +
+// DFMA: three instructions (a predicated DADD gets if-converted by ptxas
+// into DADD + two FSELs).
+#ifndef BART_SUMS_SEL
+#define BART_SUMS_SEL 1
+#endif
+__device__ __forceinline__ void add_if_eq(double &acc, uint32_t h, uint32_t slot, double v) {
+#if BART_SUMS_SEL
+  acc = __fma_rn(v, h == slot ? 1.0 : 0.0, acc);
+#else
+  if (h == slot) acc = __dadd_rn(acc, v);
+#endif
+}
+
 struct Geom {
   int m, chunk, nwords, cta, nblk, size;
   int64_t start;
@@ -208,19 +237,23 @@ struct APass {
   int ns;
 };
 
-// A pass over the register-resident chunk for slot group [base, base+NS).
-// FIRST: tree e-1's update (residuals f32 with the reference's two roundings,
-// sampler.py:755-760; cache write of the final tree).  Then the f64 residual
-// sums of tree e over its larger-tree leaves (sampler.py:556-576).
-template <int W, int NS, bool FIRST>
+// A pass over the register-resident chunk.  FIRST: tree e-1's update
+// (residuals f32 with the reference's two roundings, sampler.py:755-760;
+// cache write of the final tree).  Then the f64 residual sums of tree e over
+// its larger-tree leaves (sampler.py:556-576): with TOTAL, slots
+// [base, base+C) are accumulated by compare-and-add and the last slot ns-1
+// is the running total minus the others (one DADD per point instead of a
+// compare-and-add); without TOTAL, slots [base, base+C) only.
+template <int W, int C, bool FIRST, bool TOTAL>
 __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
                                           const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
                                           int warp, int lane, int base) {
-  uint32_t sn[NS];
-  double acc[NS];
+  uint32_t sn[C > 0 ? C : 1];
+  double acc[C > 0 ? C : 1];
+  double tot = 0.0;
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    sn[s] = base + s < A.ns ? A.slots[base + s] : 0xffffu;
+  for (int s = 0; s < C; ++s) {
+    sn[s] = base + s < (TOTAL ? A.ns - 1 : A.ns) ? A.slots[base + s] : 0xffffu;
     acc[s] = 0.0;
   }
 #pragma unroll
@@ -236,16 +269,22 @@ __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W
       for (int b = 0; b < 4; ++b) {
         const uint32_t h = (lc[k] >> (8 * b)) & 0xffu;
         const double v = (double)rv[b];
+        if (TOTAL) tot = __dadd_rn(tot, v);  // padding points (index 0) carry r = 0
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (h == sn[s]) acc[s] = __dadd_rn(acc[s], v);
+        for (int s = 0; s < C; ++s) add_if_eq(acc[s], h, sn[s], v);
       }
     }
   }
+  double rest = tot;
 #pragma unroll
-  for (int s = 0; s < NS; ++s) {
+  for (int s = 0; s < C; ++s) {
     const double v = warp_sum_f64(acc[s]);
+    if (TOTAL) rest = __dsub_rn(rest, acc[s]);
     if (lane == 0 && base + s < A.ns) S.wsum[warp][base + s] = v;
+  }
+  if (TOTAL) {  // slot ns-1 = total - others (per thread, then reduced)
+    const double v = warp_sum_f64(rest);
+    if (lane == 0) S.wsum[warp][A.ns - 1] = v;
   }
 }
 
@@ -253,15 +292,33 @@ template <int W>
 __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
                                             const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
                                             int warp, int lane) {
-  // slot-count variants {2, 4, 8} (+ 8-wide follow-up passes) keep the code
-  // a tree executes inside the instruction cache
-  if (A.ns <= 2)
-    sums_pass<W, 2, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
-  else if (A.ns <= 4)
-    sums_pass<W, 4, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
-  else
-    sums_pass<W, 8, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
-  for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+  // compared-slot variants {0, 1, 2, 3} + the total for trees of <= 4 leaves;
+  // wider trees take 8-slot passes.  Few variants: the control warp's code
+  // must stay in the instruction cache next to the workers'.
+#ifndef BART_SUMS_TOTAL
+#define BART_SUMS_TOTAL 1
+#endif
+  if (!BART_SUMS_TOTAL) {
+    if (A.ns <= 2)
+      sums_pass<W, 2, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+    else if (A.ns <= 4)
+      sums_pass<W, 4, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+    else
+      sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+    for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+    return;
+  }
+  switch (A.ns) {
+    case 1: sums_pass<W, 0, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 2: sums_pass<W, 1, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 3: sums_pass<W, 2, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 5: case 6: case 7: case 8:
+      sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    default:
+      sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
+      for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+  }
 }
 
 // x >= cut per byte (unsigned), 0x01 in every byte where it holds: 9-bit
@@ -278,6 +335,9 @@ __device__ __forceinline__ uint32_t grow4s(uint32_t l, uint32_t x, uint32_t t4, 
   return (l & ~msk) | (msk & (b4 | bytes_geu(x, c4)));
 }
 
+// Per-slot counts over the chunk: POPC of the SWAR byte-equality mask (or,
+// with BART_COUNT_POPC=0, byte-lane counters folded once per slot; measured
+// ~1% slower end to end).
 template <int W, int NS>
 __device__ __forceinline__ void count_pass(const uint32_t (&v)[W], const Geom &G, const uint8_t *slots, int ns,
                                            int base, uint32_t *wrow, int tid, int lane) {
@@ -292,12 +352,26 @@ __device__ __forceinline__ void count_pass(const uint32_t (&v)[W], const Geom &G
     const int w = tid + k * kWorkers;
     if (w < G.nwords) {
 #pragma unroll
-      for (int s = 0; s < NS; ++s) cnt[s] += __popc(bytes_eq(v[k], s4[s]));
+      for (int s = 0; s < NS; ++s) {
+#ifndef BART_COUNT_POPC
+#define BART_COUNT_POPC 1
+#endif
+#if BART_COUNT_POPC
+        cnt[s] += __popc(bytes_eq(v[k], s4[s]));
+#else
+        cnt[s] += bytes_eq(v[k], s4[s]) >> 7;
+#endif
+      }
     }
   }
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    const uint32_t cc = __reduce_add_sync(0xffffffffu, cnt[s]);
+#if BART_COUNT_POPC
+    const uint32_t mine = cnt[s];
+#else
+    const uint32_t mine = (cnt[s] * 0x01010101u) >> 24;
+#endif
+    const uint32_t cc = __reduce_add_sync(0xffffffffu, mine);
     if (lane == 0 && base + s < ns) wrow[base + s] = cc;
   }
 }
@@ -378,6 +452,29 @@ __device__ __forceinline__ void ld_poll2(const unsigned long long *p, unsigned l
   asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+// Kernel parameters the control and helper loops touch every tree, loaded
+// once into registers: reading them from the parameter (constant) bank inside
+// the loop costs a constant-cache miss -- an L2 round trip -- whenever the
+// workers' parameter reads have evicted them.
+template <typename T>
+__device__ __forceinline__ T *pin_ptr(T *p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+__device__ __forceinline__ int pin_int(int v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+struct XCtx {
+  unsigned long long *xacc, *cacc;
+  int *err;
+  int n_shards, nblk_total;
+  bool sys;
+  __device__ __forceinline__ explicit XCtx(const ChainDev &c)
+      : xacc(pin_ptr(c.xacc)), cacc(pin_ptr(c.cacc)), err(pin_ptr(c.err)), n_shards(pin_int(c.n_shards)),
+        nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0) {}
+};
+
 // Control warp, exchange X: fold the worker warps' f64 partials of ns slots
 // (fixed order), add them as fixed-point limbs into every shard's copy of set
 // X % 3.  Lane 4j+q handles word q of slot 8k+j, so each warp instruction
@@ -387,8 +484,9 @@ __device__ __forceinline__ unsigned long long pick3(const unsigned long long (&l
   return q == 0 ? l[0] : (q == 1 ? l[1] : l[2]);
 }
 
-__device__ __forceinline__ void exchange_add(const ChainDev &c, const SweepSmem &S, int ns, int set, int lane) {
-  const bool sys = c.shard_sys != 0;
+__device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx &X, const SweepSmem &S, int ns, int set,
+                                             int lane, long long *ts = nullptr) {
+  const bool sys = X.sys;
   const size_t set_off = (size_t)set * kXSetWords;
   const int q = lane & 3;
   for (int s0 = 0; s0 < ns; s0 += 8) {
@@ -401,11 +499,16 @@ __device__ __forceinline__ void exchange_add(const ChainDev &c, const SweepSmem 
       for (int step = 1; step < kWorkWarps; step <<= 1)  // fixed pairwise order
 #pragma unroll
         for (int k = 0; k + step < kWorkWarps; k += 2 * step) w[k] = __dadd_rn(w[k], w[k + step]);
+      TL_STAMP(ts && s0 == 0) ts[14] = gtimer_after(w[0]);
       unsigned long long l[3];
-      to_limbs(w[0], l, c.err);
+      to_limbs(w[0], l, X.err);
+      TL_STAMP(ts && s0 == 0) ts[15] = gtimer_after(__longlong_as_double((long long)(l[2] | l[1] | l[0])));
       if (q < 3) {
         const unsigned long long v = kTagOne | pick3(l, q);
-        for (int g = 0; g < c.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, v, sys);
+        if (X.n_shards == 1)
+          red_add(X.xacc + set_off + (size_t)s * kXSlotWords + q, v, false);
+        else
+          for (int g = 0; g < X.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, v, sys);
       }
     }
   }
@@ -421,11 +524,11 @@ __device__ __forceinline__ void ld_poll1s(const unsigned long long *p, unsigned 
 // Poll rounds [k0, k0+R) of set `set` until every used word is complete; on
 // return lane 4j (q == 0) holds in tot[k] the total of slot 8(k0+k)+j.
 template <int R>
-__device__ __forceinline__ void poll_rounds(const ChainDev &c, SweepSmem &S, int ns, int set, int k0, int lane,
-                                            double (&tot)[R]) {
-  const bool sys = c.shard_sys != 0;
-  const unsigned long long target = (unsigned long long)c.nblk_total << kTagShift;
-  const unsigned long long *base = c.xacc + (size_t)set * kXSetWords;
+__device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns, int set, int k0, int lane,
+                                            double (&tot)[R], long long *ts = nullptr) {
+  const bool sys = X.sys;
+  const unsigned long long target = (unsigned long long)X.nblk_total << kTagShift;
+  const unsigned long long *base = X.xacc + (size_t)set * kXSetWords;
   unsigned long long *prev = S.xprev[set];
   const int q = lane & 3;
   unsigned long long w[R];
@@ -447,6 +550,7 @@ __device__ __forceinline__ void poll_rounds(const ChainDev &c, SweepSmem &S, int
     }
     done = __all_sync(0xffffffffu, ok);
   } while (!done);
+  TL_STAMP(ts) ts[7] = gtimer_after(__longlong_as_double((long long)w[0]));
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     const int s = 8 * (k0 + k) + (lane >> 2);
@@ -462,16 +566,17 @@ __device__ __forceinline__ void poll_rounds(const ChainDev &c, SweepSmem &S, int
 }
 
 // Trees with <= 32 slots: returns the total of slot `lane` in every lane.
-__device__ __forceinline__ double exchange_poll_fast(const ChainDev &c, SweepSmem &S, int ns, int set, int lane) {
+__device__ __forceinline__ double exchange_poll_fast(const XCtx &X, SweepSmem &S, int ns, int set, int lane,
+                                                     long long *ts) {
   const int rounds = (ns + 7) >> 3;
   double mine = 0.0;
   if (rounds <= 1) {
     double t[1];
-    poll_rounds<1>(c, S, ns, set, 0, lane, t);
+    poll_rounds<1>(X, S, ns, set, 0, lane, t, ts);
     mine = __shfl_sync(0xffffffffu, t[0], (lane & 7) * 4);
   } else {
     double t[kFastRounds];
-    poll_rounds<kFastRounds>(c, S, ns, set, 0, lane, t);
+    poll_rounds<kFastRounds>(X, S, ns, set, 0, lane, t, ts);
 #pragma unroll
     for (int k = 0; k < kFastRounds; ++k) {
       const double v = __shfl_sync(0xffffffffu, t[k], (lane & 7) * 4);
@@ -482,10 +587,10 @@ __device__ __forceinline__ double exchange_poll_fast(const ChainDev &c, SweepSme
 }
 
 // Any number of slots, one round (8 slots) at a time: totals into S.tot_sum.
-__device__ __forceinline__ void exchange_poll_slow(const ChainDev &c, SweepSmem &S, int ns, int set, int lane) {
+__device__ __forceinline__ void exchange_poll_slow(const XCtx &X, SweepSmem &S, int ns, int set, int lane) {
   for (int k0 = 0; 8 * k0 < ns; ++k0) {
     double t[1];
-    poll_rounds<1>(c, S, ns, set, k0, lane, t);
+    poll_rounds<1>(X, S, ns, set, k0, lane, t);
     const int s = 8 * k0 + (lane >> 2);
     if ((lane & 3) == 0 && s < ns) S.tot_sum[s] = t[0];
   }
@@ -494,22 +599,26 @@ __device__ __forceinline__ void exchange_poll_slow(const ChainDev &c, SweepSmem 
 
 // Helper warp, count channel: add this CTA's per-leaf counts of tree j into
 // every shard's copy of count set j % 4 / poll the local copy until complete.
-__device__ __forceinline__ void counts_add(const ChainDev &c, const SweepSmem &S, int j, int ns, int lane) {
-  const bool sys = c.shard_sys != 0;
+__device__ __forceinline__ void counts_add(const ChainDev &c, const XCtx &X, const SweepSmem &S, int j, int ns,
+                                           int lane) {
+  const bool sys = X.sys;
   const size_t off = (size_t)(j % kCSets) * kCSetWords;
   for (int s = lane; s < ns; s += 32) {
     uint32_t cn = 0;
 #pragma unroll
     for (int k = 0; k < kWorkWarps; ++k) cn += S.wcnt[j & 1][k][s];
-    for (int g = 0; g < c.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | (unsigned long long)cn, sys);
+    if (X.n_shards == 1)
+      red_add(X.cacc + off + s, kTagOne | (unsigned long long)cn, false);
+    else
+      for (int g = 0; g < X.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | (unsigned long long)cn, sys);
   }
 }
 
-__device__ __forceinline__ void counts_poll(const ChainDev &c, SweepSmem &S, int j, int ns, int lane) {
-  const bool sys = c.shard_sys != 0;
-  const unsigned long long target = (unsigned long long)c.nblk_total << kTagShift;
+__device__ __forceinline__ void counts_poll(const XCtx &X, SweepSmem &S, int j, int ns, int lane) {
+  const bool sys = X.sys;
+  const unsigned long long target = (unsigned long long)X.nblk_total << kTagShift;
   const int set = j % kCSets;
-  const unsigned long long *base = c.cacc + (size_t)set * kCSetWords;
+  const unsigned long long *base = X.cacc + (size_t)set * kCSetWords;
   for (int s0 = 0; s0 < ns; s0 += 32) {
     const int s = s0 + lane;
     unsigned long long v = 0;
@@ -670,16 +779,17 @@ __device__ __forceinline__ void decide(SweepSmem &S, const Prep &P, Dec &Do, con
 
 // The same decision with lane s holding slot s in registers (trees whose
 // larger tree has <= 31 leaves: every depth <= 5 tree and nearly every depth-6
-// one).  Identical operations and order to decide(); the per-slot inputs are
-// loaded before the exchange completes, so after the poll the critical path
-// is one division, three shuffles and the ratio.
+// one).  Identical operations and order to decide().  Every lane evaluates
+// the acceptance test itself from the two children's totals (one shuffle
+// round on the critical path, no broadcast of the outcome), and every input
+// that does not depend on the exchange is loaded before it completes.
 struct DecIn {
-  double cadj, den, rcp, zs, cadj_l, cadj_r;
+  double cadj, den, rcp, zs;  // own slot (lane < ns)
   float oldv;
   int h;
   bool child;
-  // lane 0
-  double prec_l, prec_r, prec_p, partial, log_u, acc_u;
+  // move terms, every lane
+  double cadj_l, cadj_r, prec_l, prec_r, prec_p, rcp_l, rcp_r, rcp_p, zs_p, partial, lo_u, hi_u, acc_u;
 };
 
 __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8_t *rec, const TreeHdr hd, int lane) {
@@ -691,7 +801,6 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
   I.den = 1.0;
   I.rcp = 1.0;
   I.zs = 0.0;
-  I.cadj_l = I.cadj_r = 0.0;
   I.oldv = 0.f;
   I.h = 0;
   I.child = false;
@@ -703,58 +812,58 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
     I.h = mv.slot_node[lane];
     I.child = is_child(I.h, t, move);
     I.oldv = old_leaf[(grow && I.child) ? t : I.h];
-  } else if (lane == ns && move) {
+  }
+  if (move) {
     I.cadj_l = P.cadj[hd.slot_l];
     I.cadj_r = P.cadj[hd.slot_r];
-    I.den = P.prec_p;
-    I.rcp = P.rcp_p;
-    I.zs = P.zs_p;
-  }
-  if (lane == 0) {
     I.prec_l = P.prec_l;
     I.prec_r = P.prec_r;
     I.prec_p = P.prec_p;
+    I.rcp_l = P.rcp[hd.slot_l];
+    I.rcp_r = P.rcp[hd.slot_r];
+    I.rcp_p = P.rcp_p;
+    I.zs_p = P.zs_p;
     I.partial = P.partial;
-    I.log_u = mv.log_u;
+    I.lo_u = mv.log_u - 1e-9;
+    I.hi_u = mv.log_u + 1e-9;
     I.acc_u = mv.acc_u;
   }
 }
 
+__device__ __noinline__ bool accept_near_tie(double la, double acc_u) { return acc_u < exp(la); }
+
 __device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &I, double tot, const TreeHdr hd,
-                                            int lane, const DecConst &K) {
+                                            int lane, const DecConst &K, long long *ts) {
   const int kind = hd.kind, t = hd.node, ns = hd.nslots;
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
-  const int sl_i = hd.slot_l, sr_i = hd.slot_r;
-  const double tl = __shfl_sync(0xffffffffu, tot, sl_i), tr = __shfl_sync(0xffffffffu, tot, sr_i);
-  double num = 1.0, sums = 0.0;
-  if (lane < ns) {
-    sums = __dadd_rn(tot, I.cadj);  // sampler.py:570-576
-    num = __dadd_rn(K.prior, __dmul_rn(K.tau, sums));
-  } else if (lane == ns && move) {  // the collapsed parent (sampler.py:861-866)
-    const double sl = __dadd_rn(tl, I.cadj_l), sr = __dadd_rn(tr, I.cadj_r);
-    num = __dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr)));
-  }
-  const double q = div_rcp(num, I.den, I.rcp);
+  const double tl = __shfl_sync(0xffffffffu, tot, hd.slot_l), tr = __shfl_sync(0xffffffffu, tot, hd.slot_r);
+  // own leaf (sampler.py:570-595)
+  const double sums = __dadd_rn(tot, I.cadj);
+  const double q = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sums)), I.den, I.rcp);
   const double v = __dadd_rn(q, I.zs);
-  const double ml = __shfl_sync(0xffffffffu, q, sl_i), mr = __shfl_sync(0xffffffffu, q, sr_i);
-  const double mp = __shfl_sync(0xffffffffu, q, ns), vp = __shfl_sync(0xffffffffu, v, ns);
   int acc = 0;
-  if (move && lane == 0) {  // sum part (sampler.py:634-645) and the test (sampler.py:833-834)
+  double vp = 0.0;
+  if (move) {
+    // the children and the collapsed parent (sampler.py:861-866), then the sum
+    // part (sampler.py:634-645) and the test (sampler.py:833-834) -- in every lane
+    const double sl = __dadd_rn(tl, I.cadj_l), sr = __dadd_rn(tr, I.cadj_r);
+    const double ml = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sl)), I.prec_l, I.rcp_l);
+    const double mr = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sr)), I.prec_r, I.rcp_r);
+    const double mp = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr))), I.prec_p, I.rcp_p);
+    vp = __dadd_rn(mp, I.zs_p);
     const double t_l = __dmul_rn(__dmul_rn(ml, ml), I.prec_l);
     const double t_r = __dmul_rn(__dmul_rn(mr, mr), I.prec_r);
     const double t_p = __dmul_rn(__dmul_rn(mp, mp), I.prec_p);
     const double sum_part = __dmul_rn(0.5, __dsub_rn(__dadd_rn(t_l, t_r), t_p));
     const double la = __dmul_rn(grow ? 1.0 : -1.0, __dadd_rn(I.partial, sum_part));
-    if (la >= 0.0)
+    if (la >= 0.0 || la > I.hi_u)
       acc = 1;
-    else if (la < I.log_u - 1e-9)
+    else if (la < I.lo_u)
       acc = 0;
-    else if (la > I.log_u + 1e-9)
-      acc = 1;
     else
-      acc = I.acc_u < exp(la);
+      acc = accept_near_tie(la, I.acc_u) ? 1 : 0;
   }
-  acc = __shfl_sync(0xffffffffu, acc, 0);
+  TL_STAMP(ts) ts[10] = gtimer_after((double)acc);
   const bool fsmall = move && ((acc != 0) != grow);
   if (lane < ns) {  // residual delta (sampler.py:755-760)
     const float nv = (fsmall && I.child) ? __double2float_rn(vp) : __double2float_rn(v);
@@ -768,9 +877,14 @@ __device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &
   __syncwarp();
   named_arrive(BAR_DECISION, kBarWC);
   // for the helper's bookkeeping (off the critical path)
-  if (lane < ns) Do.sums_s[lane] = sums;
-  if (lane <= ns) Do.v_s[lane] = v;
-  if (lane == 0) Do.acc = acc;
+  if (lane < ns) {
+    Do.sums_s[lane] = sums;
+    Do.v_s[lane] = v;
+  }
+  if (lane == 0) {
+    Do.v_s[ns] = vp;
+    Do.acc = acc;
+  }
 }
 
 // Helper warp, one CTA per tree: accept flag, structure write, the new leaf
@@ -850,7 +964,7 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
     if (lane == 0) mbar_arrive(&S.cnt_mbar[0]);
   }
   for (int e = -1; e <= m; ++e) {
-    if (tl) tl[(size_t)(e + 1) * 8 + 0] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 0] = gtimer_after((double)S.flag_t);  // after the barrier releases
     // ---- A_e: critical path
     if (e >= 0 && e < m) {
       APass A;
@@ -888,7 +1002,7 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       named_arrive(BAR_PARTIALS, kBarWC);
       break;
     }
-    if (tl) tl[(size_t)(e + 1) * 8 + 1] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 1] = gtimer();
     // ---- B_e: tree e+2's refresh + counts, hidden behind the exchange
     uint32_t lnn[W];
     const int j2 = e + 2;
@@ -909,9 +1023,9 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       lc[k] = ln[k];
       ln[k] = lnn[k];
     }
-    if (tl) tl[(size_t)(e + 1) * 8 + 2] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 2] = gtimer();
     if (e >= 0) named_sync(BAR_DECISION, kBarWC);  // decision of tree e installed (S.dlt, flags)
-    if (tl) tl[(size_t)(e + 1) * 8 + 3] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 3] = gtimer();
   }
 }
 
@@ -919,6 +1033,7 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
 __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                              const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
+  const XCtx X(c);
   __syncthreads();  // prologue barrier
   for (int e = 0; e <= m; ++e) {
     const bool has_cur = e < m;
@@ -928,23 +1043,36 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
     const bool fast = ns < 32;
 
     named_sync(BAR_PARTIALS, kBarWC);  // A_e partials complete
-    if (tl) tl[(size_t)(e + 1) * 8 + 4] = gtimer();
-    if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 0] = nstimer();
-    exchange_add(c, S, ns, set, lane);
+    // (BAR.SYNC defers blocking to the next dependent instruction: stamp after a shared load)
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 4] = gtimer_after(S.wsum[0][0]);
+#if BART_TIMELINE
+    if (c.trace && lane == 0) {
+      const volatile double dep = S.wsum[0][0];
+      (void)dep;
+      c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 0] = nstimer();
+    }
+#endif
+    long long *ts = tl ? tl + (size_t)(e + 1) * 16 : nullptr;
+    exchange_add(c, X, S, ns, set, lane, ts);
+    TL_STAMP(ts) ts[5] = gtimer();
     DecIn I;
     if (has_cur) {
       mbar_wait(&S.prep_mbar[e & 1], par2(e));  // helper: prep(e) ready
       if (fast) decide_load(I, S.prep[e & 1], G.rec(e), hd, lane);
     }
+    TL_STAMP(ts) ts[6] = gtimer();
     double tot = 0.0;
     if (fast)
-      tot = exchange_poll_fast(c, S, ns, set, lane);
+      tot = exchange_poll_fast(X, S, ns, set, lane, ts);
     else
-      exchange_poll_slow(c, S, ns, set, lane);
-    if (tl) tl[(size_t)(e + 1) * 8 + 5] = gtimer();
+      exchange_poll_slow(X, S, ns, set, lane);
+    TL_STAMP(ts) ts[8] = gtimer_after(tot);
+#if BART_TIMELINE
     if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 1] = nstimer();
+#endif
     if (has_cur && fast) {
-      decide_fast(S, S.dec[e & 1], I, tot, hd, lane, K);
+      decide_fast(S, S.dec[e & 1], I, tot, hd, lane, K, ts);
+      TL_STAMP(ts) ts[11] = gtimer();
     } else {
       if (fast && lane < ns) S.tot_sum[lane] = tot;
       __syncwarp();
@@ -953,7 +1081,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
         named_arrive(BAR_DECISION, kBarWC);
       }
     }
-    if (tl) tl[(size_t)(e + 1) * 8 + 6] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 12] = gtimer();
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.dec_mbar[e & 1]);  // dec[e & 1] (or sum r^2) for the helper
   }
@@ -963,6 +1091,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                             const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
+  const XCtx X(c);
   auto issue_tree = [&](int j) {  // lane 0: cache row, split column, record -> ring slot j % kRing
     const TreeHdr hd = G.hdr[j];
     unsigned long long *mb = &S.mbar[j % kRing];
@@ -976,7 +1105,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   };
   auto prepare_tree = [&](int j) {
     mbar_wait(&S.mbar[j % kRing], (uint32_t)((j / kRing) & 1));
-    counts_poll(c, S, j, G.hdr[j].nslots, lane);
+    counts_poll(X, S, j, G.hdr[j].nslots, lane);
     prepare(S.prep[j & 1], S.hcnt, G.rec(j), G.size, G.hdr[j], lane, K);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.prep_mbar[j & 1]);
@@ -986,18 +1115,18 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   __syncthreads();  // prologue barrier
   for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
     mbar_wait(&S.cnt_mbar[j & 1], par2(j));
-    counts_add(c, S, j, G.hdr[j].nslots, lane);
+    counts_add(c, X, S, j, G.hdr[j].nslots, lane);
   }
   if (m > 0) prepare_tree(0);
   for (int e = 0; e <= m; ++e) {
     if (e + 2 < m) {  // B_e done: publish the counts of tree e+2
       mbar_wait(&S.cnt_mbar[e & 1], par2(e + 2));
-      counts_add(c, S, e + 2, G.hdr[e + 2].nslots, lane);
+      counts_add(c, X, S, e + 2, G.hdr[e + 2].nslots, lane);
     }
     // tree e+1's count-only terms: prep[(e+1)&1] was last read by decide(e-1)
     // and decide_post(e-1), both done
     if (e + 1 < m) prepare_tree(e + 1);
-    if (tl) tl[(size_t)(e + 1) * 8 + 7] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 13] = gtimer();
     mbar_wait(&S.dec_mbar[e & 1], par2(e));  // exchange e done, decision e taken
     if (e < m && G.cta == e % G.nblk) decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K);
     if (e == m && G.cta == m % G.nblk && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
@@ -1067,13 +1196,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
     K.tau_mu = __ddiv_rn(1.0, __dmul_rn(c.hp.leaf_sd, c.hp.leaf_sd));
     K.prior = __dmul_rn(K.tau_mu, c.hp.leaf_mean);
     K.lm_term = __dmul_rn(__dmul_rn(__dmul_rn(0.5, c.hp.leaf_mean), c.hp.leaf_mean), K.tau_mu);
-    long long *tl = (c.timeline && G.cta == 0 && lane == 0) ? c.timeline : nullptr;
+    long long *tl = (BART_TIMELINE && c.timeline && G.cta == 0 && lane == 0) ? c.timeline : nullptr;
     if (warp == kCtrlWarp)
       control_loop(c, S, G, lane, K, xbase, tl);
     else
       helper_loop(c, S, G, lane, K, xbase, tl);
   } else {
-    long long *tl = (c.timeline && tid == 0 && G.cta == 0) ? c.timeline : nullptr;
+    long long *tl = (BART_TIMELINE && c.timeline && tid == 0 && G.cta == 0) ? c.timeline : nullptr;
     worker_loop<W>(c, S, G, tid, warp, lane, tl);
   }
 }

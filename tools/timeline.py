@@ -7,14 +7,15 @@ Control lane 0: partials synced, exchange complete, decision published; helper: 
 import sys, os
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2410_23244_b200 import _build, _native as N
+from paper_2410_23244_b200 import _build
+os.environ["BART_LIB"] = _build.build_timeline()  # instrumented variant (BART_TIMELINE=1)
+from paper_2410_23244_b200 import _native as N
 from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
 from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 m = int(sys.argv[3]) if len(sys.argv) > 3 else 200
-_build.build()
 rng = np.random.default_rng(0)
 Xq = rng.integers(0, 101, (n, p), dtype=np.uint8)
 y = 10 * np.sin(np.pi * Xq[:, 0] * Xq[:, 1] / 1e4) + 20 * (Xq[:, 2] / 100 - .5) ** 2 + 10 * Xq[:, 3] / 100 + rng.normal(size=n)
@@ -27,17 +28,22 @@ N.check(N.lib().bart_profile(st.handle, 3, N.ptr(ms)))
 tl = np.zeros((3, m + 2, 8), np.int64)
 N.check(N.lib().bart_get_timeline(st.handle, N.ptr(tl)))
 print(f"n={n} p={p} m={m} sweep {ms[1]/3:.3f} ms/launch, {ms[1]/3/m*1e3:.2f} us/tree, propose {ms[2]/3*1e3:.1f} us; cfg {st.sweep_config()}")
-t = tl[0][1:m + 1].astype(float)  # rows for trees 0..m-1
+t = tl.reshape(-1)[: (m + 2) * 16].reshape(m + 2, 16)[1:m + 1].astype(float)  # rows: trees 0..m-1
 q = lambda a: f"{np.median(a):6.0f} (p90 {np.percentile(a, 90):6.0f})"
-print("worker  A pass          ", q(t[:, 1] - t[:, 0]))
-print("worker  B pass          ", q(t[:, 2] - t[:, 1]))
-print("worker  wait decision   ", q(t[:, 3] - t[:, 2]))
-print("control publish->synced ", q(t[:, 4] - t[:, 1]))
-print("control exchange        ", q(t[:, 5] - t[:, 4]))
-print("control decide          ", q(t[:, 6] - t[:, 5]))
-print("helper prepare done     ", q(t[:, 7] - t[:, 6]))
-print("decision -> worker      ", q(t[:, 3] - t[:, 6]))
-print("tree period (cycles)    ", q(np.diff(tl[0][1:m + 2, 0].astype(float))))
+print("worker  A pass                ", q(t[:, 1] - t[:, 0]))
+print("worker  B pass                ", q(t[:, 2] - t[:, 1]))
+print("worker0 published -> fold done", q(t[:, 14] - t[:, 1]))
+print("fold -> limbs                 ", q(t[:, 15] - t[:, 14]))
+print("limbs -> adds issued          ", q(t[:, 5] - t[:, 15]))
+print("adds -> prep loaded           ", q(t[:, 6] - t[:, 5]))
+print("prep -> poll complete         ", q(t[:, 7] - t[:, 6]))
+print("poll -> totals (gather/limbs) ", q(t[:, 8] - t[:, 7]))
+print("decide: division              ", q(t[:, 9] - t[:, 8]))
+print("decide: accept known          ", q(t[:, 10] - t[:, 9]))
+print("decide: deltas + arrive       ", q(t[:, 11] - t[:, 10]))
+print("worker: decision->A start     ", q(t[:, 0][1:] - t[:, 11][:-1]))
+print("helper prepare(e+1) done      ", q(t[:, 13] - t[:, 12]))
+print("tree period (cycles)          ", q(np.diff(t[:, 4])))
 nb = st.sweep_config()["ctas"]
 tr = np.zeros((m + 2, nb, 2), np.int64)
 N.check(N.lib().bart_get_trace(st.handle, N.ptr(tr)))
