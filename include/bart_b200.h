@@ -152,7 +152,7 @@ int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms);
 int64_t bart_kernel_launches(bart_chain *h);
 /* 1 if bart_run replays a captured CUDA graph, 0 if it falls back to launches */
 int bart_graph_active(bart_chain *h);
-int bart_sweep_config(bart_chain *h, int32_t *out /* [ctas, threads, chunk, smem_bytes] */);
+int bart_sweep_config(bart_chain *h, int32_t *out /* [ctas, threads, chunk, smem_bytes, stream] */);
 
 const char *bart_last_error(void);
 const char *bart_version(void);

@@ -193,14 +193,17 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   nblk = (int)((c.n + chunk - 1) / chunk);
   c.nblk = nblk;
   c.chunk = (int)chunk;
-  h->smem = sweep_smem_bytes(c.m, c.chunk, c.size);
-  if (sweep_words_per_thread(c.chunk) < 0 || (int64_t)h->smem > optin)
-    return bail(fail(BART_EINVAL, "n per device too large for the smem-resident sweep: chunk " +
-                                      std::to_string(chunk) + " points needs " + std::to_string(h->smem) +
-                                      " B shared memory > " + std::to_string(optin) + " (shard across GPUs)"));
+  // register mode while the chunk fits the workers' registers, else stream
+  // mode (residuals in global memory / L2, refreshed rows in Lref)
+  c.stream = sweep_words_per_thread(c.chunk) == 0 ? 1 : 0;
+  if (const char *fs = getenv("BART_FORCE_STREAM")) c.stream |= atoi(fs) != 0;  // tests: stream mode at small n
+  h->smem = sweep_smem_bytes(c.m, c.chunk, c.size, c.stream != 0);
+  if ((int64_t)h->smem > optin)
+    return bail(fail(BART_EINVAL, "sweep needs " + std::to_string(h->smem) + " B shared memory > " +
+                                      std::to_string(optin) + " (n_trees too large?)"));
   if (cudaError_t e = sweep_prepare(h->smem); e != cudaSuccess)
     return bail(fail(BART_ECUDA, std::string("sweep_prepare: ") + cudaGetErrorString(e)));
-  const int maxc = sweep_max_ctas(h->smem, device, c.chunk);
+  const int maxc = sweep_max_ctas(h->smem, device, c.chunk, c.stream != 0);
   if (maxc < nblk) return bail(fail(BART_ECUDA, "sweep grid cannot be co-resident"));
 
   const size_t np = (size_t)c.n_pad;
@@ -220,6 +223,8 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   if (e == cudaSuccess) e = own(h, &ptr, cnt)
   OWN(Xt, (size_t)c.p * np);
   OWN(L, (size_t)c.m * np);
+  uint8_t *Lref = nullptr;
+  if (c.stream) OWN(Lref, 3 * np);
   OWN(r, np);
   OWN(yy, np);
   OWN(axis, (size_t)c.m * c.half);
@@ -247,6 +252,7 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   if (e != cudaSuccess) return bail(fail(BART_ECUDA, std::string("allocation: ") + cudaGetErrorString(e)));
   c.Xt = Xt;
   c.L = L;
+  c.Lref = Lref;
   c.r = r;
   c.y = yy;
   c.axis = axis;
@@ -541,6 +547,7 @@ int bart_sweep_config(bart_chain *h, int32_t *out) {
   out[1] = kSweepThreads;
   out[2] = h->c.chunk;
   out[3] = (int32_t)h->smem;
+  out[4] = h->c.stream;
   return BART_OK;
 }
 

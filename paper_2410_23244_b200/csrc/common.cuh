@@ -115,6 +115,8 @@ struct ChainDev {
   unsigned long long *iter_dev;
   uint64_t seed;
   int nblk, chunk;
+  int stream;     // 1: chunk beyond the register budget -- residuals in global (L2) memory
+  uint8_t *Lref;  // stream mode: (3, n_pad) refreshed larger-tree rows of trees e-1, e, e+1
   long long *timeline;        // optional per-tree phase stamps (clock64), CTA 0 and last CTA
   long long *trace;           // optional (m+1, nblk, 2) globaltimer: publish, gathered
   HP hp;

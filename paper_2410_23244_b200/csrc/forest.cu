@@ -16,11 +16,13 @@
 
 namespace bart {
 
-// dst[c * dst_ld + r] = src[r * src_ld + c] for r < rows, c < cols
+// dst[c * dst_ld + r] = src[r * src_ld + c] for r < rows, c < cols; one
+// 32x32 tile per CTA over a 1-D grid (either dimension may exceed 65535 tiles)
 __global__ void transpose_u8_kernel(const uint8_t *__restrict__ src, int64_t rows, int64_t cols, int64_t src_ld,
-                                    uint8_t *__restrict__ dst, int64_t dst_ld) {
+                                    uint8_t *__restrict__ dst, int64_t dst_ld, int64_t col_tiles) {
   __shared__ uint8_t tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int64_t tr = (int64_t)blockIdx.x / col_tiles, tc = (int64_t)blockIdx.x % col_tiles;
+  const int64_t r0 = tr * 32, c0 = tc * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
   for (int k = ty; k < 32; k += 8) {
     const int64_t r = r0 + k, cc = c0 + tx;
@@ -36,8 +38,8 @@ __global__ void transpose_u8_kernel(const uint8_t *__restrict__ src, int64_t row
 void launch_transpose_u8(const uint8_t *src, int64_t rows, int64_t cols, int64_t src_ld, uint8_t *dst,
                          int64_t dst_ld, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return;
-  const dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
-  transpose_u8_kernel<<<grid, 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld);
+  const int64_t rt = (rows + 31) / 32, ct = (cols + 31) / 32;
+  transpose_u8_kernel<<<(unsigned)(rt * ct), 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
 }
 
 __global__ void fill_root_kernel(uint8_t *L, int m, int64_t n, int64_t n_pad) {

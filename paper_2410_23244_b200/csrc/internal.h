@@ -10,9 +10,9 @@
 namespace bart {
 
 void launch_propose(const ChainDev &c, int device_rng, cudaStream_t s);
-size_t sweep_smem_bytes(int m, int chunk, int size);
+size_t sweep_smem_bytes(int m, int chunk, int size, bool stream);
 cudaError_t sweep_prepare(size_t smem);
-int sweep_max_ctas(size_t smem, int device, int chunk);
+int sweep_max_ctas(size_t smem, int device, int chunk, bool stream);
 int sweep_words_per_thread(int chunk);
 int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s);
 

@@ -97,20 +97,26 @@ struct __align__(16) SweepSmem {
   int flag_wr, flag_prune, flag_t;
 };
 
-__host__ __device__ __forceinline__ size_t ring_slot_bytes(int chunk, int rstride) { return (size_t)2 * chunk + (size_t)rstride; }
-
-size_t sweep_smem_bytes(int m, int chunk, int size) {
-  size_t b = sizeof(SweepSmem);
-  b += ((size_t)m * sizeof(TreeHdr) + 15) & ~(size_t)15;
-  b += (size_t)kRing * ring_slot_bytes(chunk, rec_stride(size));
-  return b;
+// ring slot: cache row | split column | record (register mode); record only (stream mode)
+__host__ __device__ __forceinline__ size_t ring_row_bytes(int chunk, bool stream) { return stream ? 0 : (size_t)2 * chunk; }
+__host__ __device__ __forceinline__ size_t ring_slot_bytes(int chunk, int rstride, bool stream) {
+  return ring_row_bytes(chunk, stream) + (size_t)rstride;
 }
 
+// Words (4 points) per worker thread held in registers, or 0: the chunk is
+// too big and the sweep streams residuals through global memory (L2).
 int sweep_words_per_thread(int chunk) {
   const int words = (chunk + 3) / 4;
   for (int w : {1, 2, 4, 8})
     if (w * kWorkers >= words) return w;
-  return -1;
+  return 0;
+}
+
+size_t sweep_smem_bytes(int m, int chunk, int size, bool stream) {
+  size_t b = sizeof(SweepSmem);
+  b += ((size_t)m * sizeof(TreeHdr) + 15) & ~(size_t)15;
+  b += (size_t)kRing * ring_slot_bytes(chunk, rec_stride(size), stream);
+  return b;
 }
 
 // ------------------------------------------------------------ async copies, barriers
@@ -222,10 +228,11 @@ struct Geom {
   int64_t start;
   uint32_t lenp;
   uint32_t slot_bytes;  // ring slot: cache row | split column | record
+  uint32_t row_bytes;   // 2 * chunk (register mode) or 0 (stream mode)
   uint8_t *ring;
   TreeHdr *hdr;
   __device__ __forceinline__ uint8_t *slot(int j) const { return ring + (size_t)(j % kRing) * slot_bytes; }
-  __device__ __forceinline__ const uint8_t *rec(int j) const { return slot(j) + 2 * (size_t)chunk; }
+  __device__ __forceinline__ const uint8_t *rec(int j) const { return slot(j) + row_bytes; }
 };
 
 // ------------------------------------------------------------ worker passes
@@ -788,8 +795,6 @@ struct DecIn {
   float oldv;
   int h;
   bool child;
-  // move terms, every lane
-  double cadj_l, cadj_r, prec_l, prec_r, prec_p, rcp_l, rcp_r, rcp_p, zs_p, partial, lo_u, hi_u, acc_u;
 };
 
 __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8_t *rec, const TreeHdr hd, int lane) {
@@ -813,27 +818,13 @@ __device__ __forceinline__ void decide_load(DecIn &I, const Prep &P, const uint8
     I.child = is_child(I.h, t, move);
     I.oldv = old_leaf[(grow && I.child) ? t : I.h];
   }
-  if (move) {
-    I.cadj_l = P.cadj[hd.slot_l];
-    I.cadj_r = P.cadj[hd.slot_r];
-    I.prec_l = P.prec_l;
-    I.prec_r = P.prec_r;
-    I.prec_p = P.prec_p;
-    I.rcp_l = P.rcp[hd.slot_l];
-    I.rcp_r = P.rcp[hd.slot_r];
-    I.rcp_p = P.rcp_p;
-    I.zs_p = P.zs_p;
-    I.partial = P.partial;
-    I.lo_u = mv.log_u - 1e-9;
-    I.hi_u = mv.log_u + 1e-9;
-    I.acc_u = mv.acc_u;
-  }
 }
 
-__device__ __noinline__ bool accept_near_tie(double la, double acc_u) { return acc_u < exp(la); }
+__device__ __forceinline__ bool accept_near_tie(double la, double acc_u) { return acc_u < exp(la); }
 
-__device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &I, double tot, const TreeHdr hd,
-                                            int lane, const DecConst &K, long long *ts) {
+__device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &I, double tot, const Prep &P,
+                                            const uint8_t *rec, const TreeHdr hd, int lane, const DecConst &K,
+                                            long long *ts) {
   const int kind = hd.kind, t = hd.node, ns = hd.nslots;
   const bool grow = kind == KIND_GROW, move = kind != KIND_NONE;
   const double tl = __shfl_sync(0xffffffffu, tot, hd.slot_l), tr = __shfl_sync(0xffffffffu, tot, hd.slot_r);
@@ -845,23 +836,30 @@ __device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &
   double vp = 0.0;
   if (move) {
     // the children and the collapsed parent (sampler.py:861-866), then the sum
-    // part (sampler.py:634-645) and the test (sampler.py:833-834) -- in every lane
-    const double sl = __dadd_rn(tl, I.cadj_l), sr = __dadd_rn(tr, I.cadj_r);
-    const double ml = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sl)), I.prec_l, I.rcp_l);
-    const double mr = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sr)), I.prec_r, I.rcp_r);
-    const double mp = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr))), I.prec_p, I.rcp_p);
-    vp = __dadd_rn(mp, I.zs_p);
-    const double t_l = __dmul_rn(__dmul_rn(ml, ml), I.prec_l);
-    const double t_r = __dmul_rn(__dmul_rn(mr, mr), I.prec_r);
-    const double t_p = __dmul_rn(__dmul_rn(mp, mp), I.prec_p);
+    // part (sampler.py:634-645) and the test (sampler.py:833-834) -- in every
+    // lane; the move terms are warp-uniform shared loads issued alongside the
+    // shuffles
+    const TreeMove &mv = rec_hdr(rec);
+    const double cadj_l = P.cadj[hd.slot_l], cadj_r = P.cadj[hd.slot_r];
+    const double prec_l = P.prec_l, prec_r = P.prec_r, prec_p = P.prec_p;
+    const double rcp_l = P.rcp[hd.slot_l], rcp_r = P.rcp[hd.slot_r], rcp_p = P.rcp_p;
+    const double sl = __dadd_rn(tl, cadj_l), sr = __dadd_rn(tr, cadj_r);
+    const double ml = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sl)), prec_l, rcp_l);
+    const double mr = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, sr)), prec_r, rcp_r);
+    const double mp = div_rcp(__dadd_rn(K.prior, __dmul_rn(K.tau, __dadd_rn(sl, sr))), prec_p, rcp_p);
+    vp = __dadd_rn(mp, P.zs_p);
+    const double t_l = __dmul_rn(__dmul_rn(ml, ml), prec_l);
+    const double t_r = __dmul_rn(__dmul_rn(mr, mr), prec_r);
+    const double t_p = __dmul_rn(__dmul_rn(mp, mp), prec_p);
     const double sum_part = __dmul_rn(0.5, __dsub_rn(__dadd_rn(t_l, t_r), t_p));
-    const double la = __dmul_rn(grow ? 1.0 : -1.0, __dadd_rn(I.partial, sum_part));
-    if (la >= 0.0 || la > I.hi_u)
+    const double la = __dmul_rn(grow ? 1.0 : -1.0, __dadd_rn(P.partial, sum_part));
+    const double log_u = mv.log_u;
+    if (la >= 0.0 || la > log_u + 1e-9)
       acc = 1;
-    else if (la < I.lo_u)
+    else if (la < log_u - 1e-9)
       acc = 0;
     else
-      acc = accept_near_tie(la, I.acc_u) ? 1 : 0;
+      acc = accept_near_tie(la, mv.acc_u) ? 1 : 0;
   }
   TL_STAMP(ts) ts[10] = gtimer_after((double)acc);
   const bool fsmall = move && ((acc != 0) != grow);
@@ -1029,6 +1027,217 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
   }
 }
 
+// ------------------------------------------------------------ stream mode
+// Chunks beyond the register budget (n per device > ~2.2M): the residuals
+// stay in global memory, L2-resident (4n bytes: 40 MB at n = 1e7), and tree
+// j's refreshed larger-tree row goes to the global scratch ring Lref[j % 3].
+// Same passes as the register mode, over tiles of kTileW words per thread.
+constexpr int kTileW = 4;
+
+__device__ __forceinline__ const uint8_t *lref_row(const ChainDev &c, const Geom &G, int j) {
+  return c.Lref + (size_t)(j % 3) * c.n_pad + G.start;
+}
+
+// A pass (first = tree e-1's update + cache write), f64 sums of slots
+// [base, base+C) (+ running total when TOTAL) accumulated over the chunk.
+template <int C, bool TOTAL>
+__device__ __forceinline__ void stream_sums(const ChainDev &c, const Geom &G, const APass &A, const uint32_t *lp32,
+                                            const uint32_t *lc32, const float *dlt, SweepSmem &S, int tid, int warp,
+                                            int lane, int base, bool first) {
+  uint32_t sn[C > 0 ? C : 1];
+  double acc[C > 0 ? C : 1];
+  double tot = 0.0;
+#pragma unroll
+  for (int s = 0; s < C; ++s) {
+    sn[s] = base + s < (TOTAL ? A.ns - 1 : A.ns) ? A.slots[base + s] : 0xffffu;
+    acc[s] = 0.0;
+  }
+  float4 *rg = reinterpret_cast<float4 *>(c.r + G.start);
+  const bool upd = first && A.do_update;
+  for (int w0 = 0; w0 < G.nwords; w0 += kWorkers * kTileW) {
+    float4 r[kTileW];
+    uint32_t lp[kTileW], lc[kTileW];
+#pragma unroll
+    for (int k = 0; k < kTileW; ++k) {
+      const int w = w0 + tid + k * kWorkers;
+      if (w < G.nwords) {
+        r[k] = rg[w];
+        lc[k] = lc32[w];
+        lp[k] = upd ? lp32[w] : 0u;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTileW; ++k) {
+      const int w = w0 + tid + k * kWorkers;
+      if (w < G.nwords) {
+        if (upd) {
+          r[k] = update4(r[k], lp[k], dlt);
+          if (A.wr) A.gL[w] = A.prune ? collapse4(lp[k], A.t) : lp[k];
+          rg[w] = r[k];
+        }
+        const float rv[4] = {r[k].x, r[k].y, r[k].z, r[k].w};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t h = (lc[k] >> (8 * b)) & 0xffu;
+          const double v = (double)rv[b];
+          if (TOTAL) tot = __dadd_rn(tot, v);
+#pragma unroll
+          for (int s = 0; s < C; ++s) add_if_eq(acc[s], h, sn[s], v);
+        }
+      }
+    }
+  }
+  double rest = tot;
+#pragma unroll
+  for (int s = 0; s < C; ++s) {
+    const double v = warp_sum_f64(acc[s]);
+    if (TOTAL) rest = __dsub_rn(rest, acc[s]);
+    if (lane == 0 && base + s < A.ns) S.wsum[warp][base + s] = v;
+  }
+  if (TOTAL) {
+    const double v = warp_sum_f64(rest);
+    if (lane == 0) S.wsum[warp][A.ns - 1] = v;
+  }
+}
+
+__device__ __forceinline__ void stream_sums_all(const ChainDev &c, const Geom &G, const APass &A, const uint32_t *lp32,
+                                                const uint32_t *lc32, const float *dlt, SweepSmem &S, int tid, int warp,
+                                                int lane) {
+  switch (A.ns) {
+    case 1: stream_sums<0, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
+    case 2: stream_sums<1, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
+    case 3: stream_sums<2, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
+    case 4: stream_sums<3, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
+    default:  // wide trees: further passes re-read the (updated) residuals
+      stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true);
+      for (int base = 8; base < A.ns; base += 8)
+        stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, base, false);
+  }
+}
+
+// B pass: tree j's row from global memory -> grow refresh -> Lref[j % 3], and
+// per-slot counts of slots [base, base+NS).
+template <int NS>
+__device__ __forceinline__ void stream_refresh_count(const ChainDev &c, const Geom &G, int j, const TreeHdr hd,
+                                                     const uint8_t *slots, uint32_t *wrow, int tid, int lane,
+                                                     int base, bool write) {
+  const uint32_t *L32 = reinterpret_cast<const uint32_t *>(c.L + (size_t)j * c.n_pad + G.start);
+  const uint32_t *X32 = reinterpret_cast<const uint32_t *>(c.Xt + (size_t)hd.axis * c.n_pad + G.start);
+  uint32_t *O32 = reinterpret_cast<uint32_t *>(const_cast<uint8_t *>(lref_row(c, G, j)));
+  const bool g = hd.kind == KIND_GROW;
+  const uint32_t t4 = 0x01010101u * hd.node, c4 = 0x01010101u * hd.cut, b4 = 0x01010101u * (2u * hd.node);
+  const int ns = hd.nslots;
+  uint32_t cnt[NS], s4[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    s4[s] = base + s < ns ? 0x01010101u * (uint32_t)slots[base + s] : 0xffffffffu;
+    cnt[s] = 0u;
+  }
+  for (int w0 = 0; w0 < G.nwords; w0 += kWorkers * kTileW) {
+    uint32_t l[kTileW], x[kTileW];
+#pragma unroll
+    for (int k = 0; k < kTileW; ++k) {
+      const int w = w0 + tid + k * kWorkers;
+      l[k] = 0u;
+      x[k] = 0u;
+      if (w < G.nwords) {
+        l[k] = write ? L32[w] : O32[w];
+        if (write && g) x[k] = X32[w];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTileW; ++k) {
+      const int w = w0 + tid + k * kWorkers;
+      if (w < G.nwords) {
+        if (write) {
+          if (g) l[k] = grow4s(l[k], x[k], t4, c4, b4);
+          O32[w] = l[k];
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) cnt[s] += __popc(bytes_eq(l[k], s4[s]));
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t cc = __reduce_add_sync(0xffffffffu, cnt[s]);
+    if (lane == 0 && base + s < ns) wrow[base + s] = cc;
+  }
+}
+
+__device__ __forceinline__ void stream_refresh_count_all(const ChainDev &c, const Geom &G, int j, const TreeHdr hd,
+                                                         const uint8_t *slots, uint32_t *wrow, int tid, int lane) {
+  const int ns = hd.nslots;
+  if (ns <= 2)
+    stream_refresh_count<2>(c, G, j, hd, slots, wrow, tid, lane, 0, true);
+  else if (ns <= 4)
+    stream_refresh_count<4>(c, G, j, hd, slots, wrow, tid, lane, 0, true);
+  else
+    for (int base = 0; base < ns; base += 8)  // later groups re-read the refreshed row
+      stream_refresh_count<8>(c, G, j, hd, slots, wrow, tid, lane, base, base == 0);
+}
+
+__device__ __forceinline__ void stream_worker_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int tid, int warp,
+                                                   int lane) {
+  __syncthreads();  // prologue barrier
+  const int m = G.m;
+  if (m > 0) {
+    mbar_wait(&S.mbar[0], 0u);
+    stream_refresh_count_all(c, G, 0, G.hdr[0], rec_hdr(G.rec(0)).slot_node, S.wcnt[0][warp], tid, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.cnt_mbar[0]);
+  }
+  for (int e = -1; e <= m; ++e) {
+    if (e >= 0 && e < m) {
+      APass A;
+      A.do_update = e > 0;
+      A.wr = e > 0 && S.flag_wr;
+      A.prune = e > 0 && S.flag_prune;
+      A.t = (uint32_t)S.flag_t;
+      A.gL = reinterpret_cast<uint32_t *>(c.L + (size_t)(e > 0 ? e - 1 : 0) * c.n_pad + G.start);
+      A.slots = rec_hdr(G.rec(e)).slot_node;
+      A.ns = G.hdr[e].nslots;
+      stream_sums_all(c, G, A, reinterpret_cast<const uint32_t *>(lref_row(c, G, e > 0 ? e - 1 : 0)),
+                      reinterpret_cast<const uint32_t *>(lref_row(c, G, e)), S.dlt, S, tid, warp, lane);
+      named_arrive(BAR_PARTIALS, kBarWC);
+    } else if (e == m) {  // tree m-1's update, sum of squares (sampler.py:790-794)
+      const bool wr = m > 0 && S.flag_wr, prune = S.flag_prune;
+      const uint32_t t = (uint32_t)S.flag_t;
+      uint32_t *gL = reinterpret_cast<uint32_t *>(c.L + (size_t)(m > 0 ? m - 1 : 0) * c.n_pad + G.start);
+      const uint32_t *lp32 = reinterpret_cast<const uint32_t *>(lref_row(c, G, m > 0 ? m - 1 : 0));
+      float4 *rg = reinterpret_cast<float4 *>(c.r + G.start);
+      double ss = 0.0;
+      for (int w = tid; w < G.nwords; w += kWorkers) {
+        float4 r = rg[w];
+        if (m > 0) {
+          const uint32_t lp = lp32[w];
+          r = update4(r, lp, S.dlt);
+          if (wr) gL[w] = prune ? collapse4(lp, t) : lp;
+          rg[w] = r;
+        }
+        const double a = r.x, b = r.y, cc = r.z, d = r.w;
+        ss = __dadd_rn(ss, __dmul_rn(a, a));
+        ss = __dadd_rn(ss, __dmul_rn(b, b));
+        ss = __dadd_rn(ss, __dmul_rn(cc, cc));
+        ss = __dadd_rn(ss, __dmul_rn(d, d));
+      }
+      const double v = warp_sum_f64(ss);
+      if (lane == 0) S.wsum[warp][0] = v;
+      named_arrive(BAR_PARTIALS, kBarWC);
+      break;
+    }
+    const int j2 = e + 2;
+    if (j2 < m) {
+      mbar_wait(&S.mbar[j2 % kRing], (uint32_t)((j2 / kRing) & 1));
+      stream_refresh_count_all(c, G, j2, G.hdr[j2], rec_hdr(G.rec(j2)).slot_node, S.wcnt[j2 & 1][warp], tid, lane);
+      fence_proxy_async();  // generic reads of the record before its slot's next TMA refill
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.cnt_mbar[j2 & 1]);
+    }
+    if (e >= 0) named_sync(BAR_DECISION, kBarWC);
+  }
+}
+
 // Control warp: exchange and decision, nothing else.
 __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                              const DecConst &K, unsigned long long xbase, long long *tl) {
@@ -1071,7 +1280,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
     if (c.trace && lane == 0) c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 1] = nstimer();
 #endif
     if (has_cur && fast) {
-      decide_fast(S, S.dec[e & 1], I, tot, hd, lane, K, ts);
+      decide_fast(S, S.dec[e & 1], I, tot, S.prep[e & 1], G.rec(e), hd, lane, K, ts);
       TL_STAMP(ts) ts[11] = gtimer();
     } else {
       if (fast && lane < ns) S.tot_sum[lane] = tot;
@@ -1098,10 +1307,15 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     uint8_t *dst = G.slot(j);
     const bool g = hd.kind == KIND_GROW;
     const uint32_t rb = (uint32_t)c.rstride;
+    if (G.row_bytes == 0) {  // stream mode: the workers read the rows from global memory
+      mbar_expect(mb, rb);
+      bulk_g2s(dst, c.rec + (size_t)j * rb, rb, mb);
+      return;
+    }
     mbar_expect(mb, (g ? 2u * G.lenp : G.lenp) + rb);
     bulk_g2s(dst, c.L + (size_t)j * c.n_pad + G.start, G.lenp, mb);
     if (g) bulk_g2s(dst + G.chunk, c.Xt + (size_t)hd.axis * c.n_pad + G.start, G.lenp, mb);
-    bulk_g2s(dst + 2 * (size_t)G.chunk, c.rec + (size_t)j * rb, rb, mb);
+    bulk_g2s(dst + G.row_bytes, c.rec + (size_t)j * rb, rb, mb);
   };
   auto prepare_tree = [&](int j) {
     mbar_wait(&S.mbar[j % kRing], (uint32_t)((j / kRing) & 1));
@@ -1157,7 +1371,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   G.size = c.size;
   G.hdr = reinterpret_cast<TreeHdr *>(smem_raw + sizeof(SweepSmem));
   G.ring = smem_raw + sizeof(SweepSmem) + ((((size_t)c.m * sizeof(TreeHdr)) + 15) & ~(size_t)15);
-  G.slot_bytes = (uint32_t)ring_slot_bytes(c.chunk, c.rstride);
+  G.row_bytes = (uint32_t)ring_row_bytes(c.chunk, W == 0);
+  G.slot_bytes = (uint32_t)ring_slot_bytes(c.chunk, c.rstride, W == 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   G.cta = blockIdx.x;
   G.nblk = gridDim.x;
@@ -1203,13 +1418,17 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
       helper_loop(c, S, G, lane, K, xbase, tl);
   } else {
     long long *tl = (BART_TIMELINE && c.timeline && tid == 0 && G.cta == 0) ? c.timeline : nullptr;
-    worker_loop<W>(c, S, G, tid, warp, lane, tl);
+    if constexpr (W == 0)
+      stream_worker_loop(c, S, G, tid, warp, lane);
+    else
+      worker_loop<W>(c, S, G, tid, warp, lane, tl);
   }
 }
 
 typedef void (*SweepFn)(ChainDev);
 static SweepFn sweep_fn(int W) {
   switch (W) {
+    case 0: return sweep_kernel<0>;
     case 1: return sweep_kernel<1>;
     case 2: return sweep_kernel<2>;
     case 4: return sweep_kernel<4>;
@@ -1228,14 +1447,14 @@ int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, sweep_fn(sweep_words_per_thread(c.chunk)), c);
+  return (int)cudaLaunchKernelEx(&cfg, sweep_fn(c.stream ? 0 : sweep_words_per_thread(c.chunk)), c);
 }
 
 cudaError_t sweep_prepare(size_t smem) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  for (int W : {1, 2, 4, 8}) {
+  for (int W : {0, 1, 2, 4, 8}) {
     cudaError_t e = cudaFuncSetAttribute(sweep_fn(W), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          optin > (int)smem ? optin : (int)smem);
     if (e != cudaSuccess) return e;
@@ -1243,9 +1462,9 @@ cudaError_t sweep_prepare(size_t smem) {
   return cudaSuccess;
 }
 
-int sweep_max_ctas(size_t smem, int device, int chunk) {
+int sweep_max_ctas(size_t smem, int device, int chunk, bool stream) {
   int per_sm = 0, sms = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fn(sweep_words_per_thread(chunk)), kSweepThreads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fn(stream ? 0 : sweep_words_per_thread(chunk)), kSweepThreads,
                                                     smem) != cudaSuccess)
     return -1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;

@@ -362,9 +362,10 @@ class SamplerState:
         return int(N.lib().bart_kernel_launches(self._h))
 
     def sweep_config(self) -> dict:
-        out = np.zeros(4, np.int32)
+        out = np.zeros(5, np.int32)
         N.check(N.lib().bart_sweep_config(self._h, N.ptr(out)))
-        return dict(ctas=int(out[0]), threads=int(out[1]), chunk=int(out[2]), smem_bytes=int(out[3]))
+        return dict(ctas=int(out[0]), threads=int(out[1]), chunk=int(out[2]), smem_bytes=int(out[3]),
+                    stream=bool(out[4]))
 
     def sync(self) -> None:
         N.check(N.lib().bart_sync(self._h))

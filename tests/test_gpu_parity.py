@@ -73,6 +73,13 @@ def test_step_matches_reference_golden(case):
     st.close()
 
 
+@pytest.mark.parametrize("case", ["a8", "wide", "depth8"])
+def test_golden_stream_mode(case, monkeypatch):
+    """The stream-mode sweep (large n) against the reference's golden steps."""
+    monkeypatch.setenv("BART_FORCE_STREAM", "1")
+    test_step_matches_reference_golden(case)
+
+
 @pytest.mark.parametrize("case", ["a8", "friedman", "wide", "depth8"])
 def test_first_step_bitwise(case):
     """From an identical start, one step reproduces the reference bit for bit."""
@@ -127,8 +134,17 @@ def test_forest_kernels_match_reference(case):
     np.testing.assert_array_equal(evaluate_forest(f, d["X"]), d["yhat"])
 
 
-def test_chain_matches_oracle_friedman_multi_cta():
-    """n=20000 spans many CTAs: 5 steps vs the oracle with the same injected randoms."""
+@pytest.fixture(params=["register", "stream"])
+def sweep_mode(request, monkeypatch):
+    """Run a test in both sweep modes: register-resident points (the default at
+    these sizes) and the stream mode large n uses, forced at small n."""
+    if request.param == "stream":
+        monkeypatch.setenv("BART_FORCE_STREAM", "1")
+    return request.param
+
+
+def test_chain_matches_oracle_friedman_multi_cta(sweep_mode):
+    """n=20000 spans many CTAs: 12 steps vs the oracle with the same injected randoms."""
     from paper_2410_23244_b200.dgp import friedman1
     from paper_2410_23244_b200.grid import build_grid_uniform, quantize
     from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
@@ -140,6 +156,7 @@ def test_chain_matches_oracle_friedman_multi_cta():
     y32 = ys.forward(y).astype(np.float32)
     st = init_state(Xq, g.counts, y32, hp, None)
     assert st.sweep_config()["ctas"] > 1
+    assert st.sweep_config()["stream"] == (sweep_mode == "stream")
     st.enable_taps(True)
     ora = OracleChain(Xq, g.counts, y32, hp)
     rng = np.random.default_rng(0)
@@ -161,7 +178,7 @@ def test_chain_matches_oracle_friedman_multi_cta():
 
 
 @pytest.mark.parametrize("n", [1, 7, 16, 17, 1025, 4099])
-def test_ragged_sizes(n):
+def test_ragged_sizes(n, sweep_mode):
     """Chunk edges: n not a multiple of 16, a single point, several CTAs."""
     from paper_2410_23244_b200.sampler import Hyperparams, StepRandoms, init_state, step
     rng = np.random.default_rng(n)
@@ -178,4 +195,29 @@ def test_ragged_sizes(n):
         np.testing.assert_array_equal(st.last_accepted, ora.last_accepted)
         np.testing.assert_array_equal(st.leaf_index, ora.leaf_index)
         np.testing.assert_allclose(st.resid, ora.resid, rtol=1e-5, atol=1e-5)
+    st.close()
+
+
+def test_stream_mode_large_n_invariants():
+    """n = 3e6 exceeds the register budget (stream mode by default): after a
+    few device-RNG steps the cache equals a fresh traversal of the forest and
+    the residuals equal y minus the forest's prediction (sampler.py:125-130)."""
+    from paper_2410_23244_b200.dgp import friedman1_binned
+    from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
+    from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
+    from paper_2410_23244_b200.trees import evaluate_forest, traverse_forest
+    n = 3_000_000
+    Xq, y, _, grid = friedman1_binned(n, 10, seed=4)
+    hp, ys = derive_hyperparams(y, FitConfig(n_trees=50))
+    y32 = ys.forward(y).astype(np.float32)
+    st = init_state(Xq, grid.counts, y32, hp, DeviceRNG(9))
+    assert st.sweep_config()["stream"]
+    run(st, hp, 6)
+    f = st.forest
+    sub = np.random.default_rng(0).choice(n, 20000, replace=False)
+    np.testing.assert_array_equal(st.leaf_index[sub], traverse_forest(f, Xq[sub]))
+    pred = evaluate_forest(f, Xq[sub])
+    np.testing.assert_allclose(st.resid[sub], (y32[sub] - pred).astype(np.float32), atol=1e-4)
+    assert 0 < st.sigma2 < 10
+    assert (f.cutpoint > 0).sum() > 0
     st.close()
