@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: shard ONE chain's points across the ranks (in-kernel NVLink exchange, strong "
+                         "scaling; BASELINE configs[3] with --n 10000000) instead of independent replicas")
     return ap.parse_args()
 
 
@@ -226,8 +229,18 @@ def run_ours(args):
     from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run, step
 
     Xq, max_cuts, y32, hp = workload(args)
-    # replicas: every rank runs an independent chain of the full workload
-    st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local)
+    sharded = args.shard and world > 1
+    if sharded:
+        # one chain: this rank holds a contiguous slice of the points; same
+        # device seed everywhere, so every shard takes identical decisions
+        from paper_2410_23244_b200.shard import ShardPlan, init_sharded_state, torch_all_gather
+        plan = ShardPlan(args.n, world)
+        lo, hi = plan.bounds(rank)
+        st = init_sharded_state(Xq[lo:hi], max_cuts, y32[lo:hi], hp, DeviceRNG(1000), plan, rank,
+                                float(np.var(y32, ddof=1)), torch_all_gather(), device=local)
+    else:
+        # replicas: every rank runs an independent chain of the full workload
+        st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local)
     cfg = st.sweep_config()
     run(st, hp, args.warmup)
     st.sync()
@@ -240,7 +253,7 @@ def run_ours(args):
     st._after_step(args.steps)
     barrier(world)
     t_max = allreduce_max(float(ms[0]) / 1e3, world)
-    value = world * args.steps / t_max
+    value = (1 if sharded else world) * args.steps / t_max
 
     # per-kernel durations (events around each launch, not graph-replayed)
     prof = np.zeros(3, np.float32)
@@ -254,7 +267,7 @@ def run_ours(args):
     achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
 
     # e2e through the reference-facing call with host random blocks
-    rng = np.random.default_rng(rank)
+    rng = np.random.default_rng(0 if sharded else rank)  # shards must inject identical random blocks
     m, size = args.m, 1 << args.depth
     h2d = 8 * (5 * m + m + m * size) + 8
     d2h = m + 8
@@ -265,7 +278,7 @@ def run_ours(args):
         _ = st.last_accepted
         _ = st.sigma2
     e2e_s = allreduce_max(time.perf_counter() - t0, world)
-    e2e = world * args.e2e_steps / e2e_s
+    e2e = (1 if sharded else world) * args.e2e_steps / e2e_s
     graph = bool(N.lib().bart_graph_active(st.handle))
     st.close()
 
@@ -280,9 +293,12 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 resid / f64 sums / u8 indices",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f32 resid / f64 sums / u8 indices",
             "data": "synthetic Friedman #1 (binned uint8), device Philox RNG",
-            "config": config_dict(args, "replicas" if world > 1 else "single chain, 1 GPU"),
+            "config": config_dict(args, (f"one chain n-sharded over {world} GPUs (in-kernel NVLink exchange)"
+                                         if sharded else (f"{world} independent chains (replicas)" if world > 1
+                                                          else "single chain, 1 GPU"))),
             "e2e": {"value": e2e, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "sampler.step(state, hp, rng=numpy Generator): host StepRandoms + H2D + step + "
                             "D2H last_accepted/sigma2"},

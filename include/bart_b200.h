@@ -76,6 +76,26 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
                 int device, bart_chain **out);
 int bart_destroy(bart_chain *h);
 
+/* ---- n-sharding across GPUs (the reference has none: PAPER.md:405-409) ----
+ * One process per GPU holds the contiguous points [offset, offset + dims->n) of
+ * a chain of n_total points; forest, proposals and random draws are replicated
+ * (seed identical on every shard), so every shard takes identical decisions.
+ * The per-tree leaf statistics travel inside the sweep kernel: each shard adds
+ * its fixed-point partials into every shard's exchange words over NVLink
+ * (peer-mapped with CUDA IPC) and polls its own copy.  Protocol:
+ *   bart_create_shard on every rank -> bart_shard_export -> all-gather the
+ *   handles (any host transport, e.g. torch.distributed) -> bart_shard_connect
+ *   with the n_shards handles in shard order -> bart_step / bart_run. */
+#define BART_SHARD_HANDLE_BYTES 256
+int bart_create_shard(const bart_dims *dims /* n = this shard's points */, int64_t n_total, int shard,
+                      int n_shards, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
+                      const float *y, double sigma2, uint64_t seed, int device, bart_chain **out);
+int bart_shard_export(bart_chain *h, void *out /* BART_SHARD_HANDLE_BYTES */);
+int bart_shard_connect(bart_chain *h, const void *all /* n_shards * BART_SHARD_HANDLE_BYTES, shard order */);
+/* Test hook: emulate `groups` shards inside one launch on one device (CTA c
+ * polls copy c % groups; every CTA adds into every copy). */
+int bart_set_copy_groups(bart_chain *h, int groups);
+
 /* Direct state edit + SamplerState.rebuild_structure_caches (sampler.py:157-168,
  * tests/util.py:11-24).  axis (m, 2^(D-1)) as uint16; leaf_index (n, m) or NULL
  * (then recomputed by traversal); resid (n,) or NULL (then y - forest in f64,

@@ -17,6 +17,7 @@ from ._build import LIB
 
 BART_OK, BART_EINVAL, BART_ECUDA, BART_ESTATE = 0, 1, 2, 3
 MAX_DEPTH = 8
+SHARD_HANDLE_BYTES = 256
 PROPOSAL_ROWS = 12
 
 
@@ -40,6 +41,11 @@ _P = C.c_void_p
 _SIGS = {
     "bart_create": [C.POINTER(Dims), C.POINTER(HParams), _P, _P, _P, C.c_double, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)],
     "bart_destroy": [_P],
+    "bart_create_shard": [C.POINTER(Dims), C.c_int64, C.c_int, C.c_int, C.POINTER(HParams), _P, _P, _P, C.c_double,
+                          C.c_uint64, C.c_int, C.POINTER(C.c_void_p)],
+    "bart_shard_export": [_P, _P],
+    "bart_shard_connect": [_P, _P],
+    "bart_set_copy_groups": [_P, C.c_int],
     "bart_set_state": [_P, _P, _P, _P, _P, _P, C.c_double],
     "bart_set_hparams": [_P, C.POINTER(HParams)],
     "bart_set_sigma2": [_P, C.c_double],

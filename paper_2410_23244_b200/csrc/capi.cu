@@ -86,6 +86,8 @@ struct bart_chain {
   cudaGraphExec_t graph = nullptr;
   bool graph_failed = false;
   std::vector<void *> owned;
+  std::vector<void *> ipc_opened;  // peer shards' exchange buffers (cudaIpcOpenMemHandle)
+  bool shard_pending = false;      // created as a shard, not yet connected
 };
 
 namespace {
@@ -94,6 +96,7 @@ void free_chain(bart_chain *h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : h->owned)
     if (p) cudaFree(p);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -153,9 +156,13 @@ extern "C" {
 const char *bart_last_error(void) { return g_err.c_str(); }
 const char *bart_version(void) { return "bart_b200 0.1 sm_100a"; }
 
-int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
-                const float *y, double sigma2, uint64_t seed, int device, bart_chain **out) {
+static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_shards, const bart_hparams *hp,
+                       const uint8_t *X, const int64_t *max_cuts, const float *y, double sigma2, uint64_t seed,
+                       int device, bart_chain **out) {
   if (int rc = check_dims(dims)) return rc;
+  if (n_shards < 1 || n_shards > kMaxShards || shard < 0 || shard >= n_shards)
+    return fail(BART_EINVAL, "shard must be in [0, n_shards), n_shards in [1, " + std::to_string(kMaxShards) + "]");
+  if (n_total < dims->n) return fail(BART_EINVAL, "n_total < points of this shard");
   if (!hp || !X || !max_cuts || !y || !out) return fail(BART_EINVAL, "NULL argument");
   for (int a = 0; a < dims->p; ++a)
     if (max_cuts[a] < 0 || max_cuts[a] > 255)
@@ -274,6 +281,15 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   c.n_shards = 1;
   c.nblk_total = c.nblk;
   c.shard_sys = 0;
+  c.copy_base = shard;
+  c.copy_groups = 1;
+  c.n_total = n_total;
+  if (n_shards > 1) {  // peers come with bart_shard_connect
+    c.n_shards = n_shards;
+    c.xpeer[shard] = xacc;
+    c.cpeer[shard] = cacc;
+    h->shard_pending = true;
+  }
   c.xsnap = xsnap;
   c.err = errf;
   c.cacc = cacc;
@@ -311,6 +327,106 @@ int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
   if (cudaStreamSynchronize(h->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess)
     return bail(fail(BART_ECUDA, "init kernels failed"));
   *out = h;
+  return BART_OK;
+}
+
+int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
+                const float *y, double sigma2, uint64_t seed, int device, bart_chain **out) {
+  return create_impl(dims, dims ? dims->n : 0, 0, 1, hp, X, max_cuts, y, sigma2, seed, device, out);
+}
+
+int bart_create_shard(const bart_dims *dims, int64_t n_total, int shard, int n_shards, const bart_hparams *hp,
+                      const uint8_t *X, const int64_t *max_cuts, const float *y, double sigma2, uint64_t seed,
+                      int device, bart_chain **out) {
+  return create_impl(dims, n_total, shard, n_shards, hp, X, max_cuts, y, sigma2, seed, device, out);
+}
+
+namespace {
+struct ShardHandle {  // what one shard tells the others (bart_shard_export)
+  cudaIpcMemHandle_t xacc, cacc;
+  int32_t nblk, shard, n_shards, magic;
+  int64_t n_local, n_total;
+};
+static_assert(sizeof(ShardHandle) <= BART_SHARD_HANDLE_BYTES, "handle size");
+constexpr int32_t kShardMagic = 0x42415254;  // "BART"
+}  // namespace
+
+int bart_shard_export(bart_chain *h, void *out) {
+  if (!h || !out) return fail(BART_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ShardHandle sh{};
+  CUDA_TRY(cudaIpcGetMemHandle(&sh.xacc, h->c.xpeer[h->c.copy_base]));
+  CUDA_TRY(cudaIpcGetMemHandle(&sh.cacc, h->c.cpeer[h->c.copy_base]));
+  sh.nblk = h->c.nblk;
+  sh.shard = h->c.copy_base;
+  sh.n_shards = h->c.n_shards;
+  sh.magic = kShardMagic;
+  sh.n_local = h->c.n;
+  sh.n_total = h->c.n_total;
+  std::memset(out, 0, BART_SHARD_HANDLE_BYTES);
+  std::memcpy(out, &sh, sizeof(sh));
+  return BART_OK;
+}
+
+int bart_shard_connect(bart_chain *h, const void *all) {
+  if (!h || !all) return fail(BART_EINVAL, "NULL argument");
+  if (!h->shard_pending) return fail(BART_ESTATE, "not an unconnected shard (bart_create_shard)");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  int total = 0;
+  int64_t points = 0;
+  for (int g = 0; g < c.n_shards; ++g) {
+    ShardHandle sh;
+    std::memcpy(&sh, static_cast<const uint8_t *>(all) + (size_t)g * BART_SHARD_HANDLE_BYTES, sizeof(sh));
+    if (sh.magic != kShardMagic || sh.shard != g || sh.n_shards != c.n_shards || sh.n_total != c.n_total)
+      return fail(BART_EINVAL, "shard handle " + std::to_string(g) + " does not belong to this chain");
+    total += sh.nblk;
+    points += sh.n_local;
+    if (g == c.copy_base) continue;
+    void *px = nullptr, *pc = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&px, sh.xacc, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened.push_back(px);
+    CUDA_TRY(cudaIpcOpenMemHandle(&pc, sh.cacc, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened.push_back(pc);
+    c.xpeer[g] = static_cast<unsigned long long *>(px);
+    c.cpeer[g] = static_cast<unsigned long long *>(pc);
+  }
+  if (points != c.n_total) return fail(BART_EINVAL, "shards cover " + std::to_string(points) + " points, n_total " +
+                                                        std::to_string(c.n_total));
+  if (total >= 2048) return fail(BART_EINVAL, "too many CTAs over all shards for the exchange tags");
+  c.nblk_total = total;
+  c.shard_sys = 1;
+  h->shard_pending = false;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return BART_OK;
+}
+
+int bart_set_copy_groups(bart_chain *h, int groups) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  ChainDev &c = h->c;
+  if (c.n_shards != 1 || h->iteration != 0)
+    return fail(BART_ESTATE, "copy groups are set on a fresh, unsharded chain");
+  if (groups < 1 || groups > kMaxShards || groups > c.nblk)
+    return fail(BART_EINVAL, "groups must be in [1, min(8, CTAs)]");
+  CUDA_TRY(cudaSetDevice(h->device));
+  for (int g = 1; g < groups; ++g) {
+    unsigned long long *x = nullptr, *cc = nullptr;
+    CUDA_TRY(own(h, &x, (size_t)kXSets * kXSetWords));
+    CUDA_TRY(own(h, &cc, (size_t)kCSets * kCSetWords));
+    c.xpeer[g] = x;
+    c.cpeer[g] = cc;
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  c.n_shards = groups;
+  c.copy_groups = groups;
+  c.copy_base = 0;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
   return BART_OK;
 }
 
@@ -374,6 +490,7 @@ int bart_set_state(bart_chain *h, const uint16_t *axis, const uint8_t *cutpoint,
 
 int bart_step(bart_chain *h, const bart_randoms *rnd) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
+  if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
   if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
@@ -404,6 +521,7 @@ int bart_propose(bart_chain *h, const double *move_u) {
 
 int bart_run(bart_chain *h, int64_t n_iter) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
+  if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
   if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   ensure_graph(h);

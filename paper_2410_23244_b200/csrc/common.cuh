@@ -103,9 +103,12 @@ struct ChainDev {
   int taps;
   unsigned long long *xacc;     // this shard's exchange sets [kXSets][kXSetWords] (polled)
   unsigned long long *xpeer[kMaxShards];  // every shard's xacc (own included): where partials are added
-  int n_shards;                 // copies in xpeer
+  int n_shards;                 // copies in xpeer (= shards of the chain)
   int nblk_total;               // CTAs over all shards = arrival tag of a complete word
-  int shard_sys;                // 1: peers on other devices (system-scope fences)
+  int shard_sys;                // 1: peers on other devices (system-scope atomics and polls)
+  int copy_base, copy_groups;   // CTA c polls copy copy_base + c % copy_groups (copy_groups > 1 only
+                                // when one launch emulates several shards on one device)
+  int64_t n_total;              // points of the whole chain (chi-square df, sampler.py:259)
   int *err;                     // device error flags (bit 0: exchange value out of fixed-point range)
   unsigned long long *xsnap;    // [1 + kXSets*(kSlotsMax+1)*4]: exchange count, then every polled
                                 // word's last complete value (the next sweep's baseline)

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kProposeWarps * 32) propose_kernel(ChainDev c,
   const uint2 key = make_uint2((uint32_t)c.seed, (uint32_t)(c.seed >> 32));
 
   if (device_rng && blockIdx.x == gridDim.x - 1) {  // the chi-square block
-    if (threadIdx.x == 0) *c.rand_chi2 = chi2_draw(c.hp.nu + (double)c.n, it, key);
+    if (threadIdx.x == 0) *c.rand_chi2 = chi2_draw(c.hp.nu + (double)c.n_total, it, key);
     return;
   }
   const int j = blockIdx.x * kProposeWarps + wl;

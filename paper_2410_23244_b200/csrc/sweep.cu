@@ -477,9 +477,11 @@ struct XCtx {
   int *err;
   int n_shards, nblk_total;
   bool sys;
-  __device__ __forceinline__ explicit XCtx(const ChainDev &c)
-      : xacc(pin_ptr(c.xacc)), cacc(pin_ptr(c.cacc)), err(pin_ptr(c.err)), n_shards(pin_int(c.n_shards)),
-        nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0) {}
+  // xacc/cacc: the copy this CTA polls
+  __device__ __forceinline__ XCtx(const ChainDev &c, int cta)
+      : xacc(pin_ptr(c.copy_groups > 1 ? c.xpeer[c.copy_base + cta % c.copy_groups] : c.xacc)),
+        cacc(pin_ptr(c.copy_groups > 1 ? c.cpeer[c.copy_base + cta % c.copy_groups] : c.cacc)), err(pin_ptr(c.err)),
+        n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0) {}
 };
 
 // Control warp, exchange X: fold the worker warps' f64 partials of ns slots
@@ -1242,7 +1244,7 @@ __device__ __forceinline__ void stream_worker_loop(const ChainDev &c, SweepSmem 
 __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                              const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
-  const XCtx X(c);
+  const XCtx X(c, G.cta);
   __syncthreads();  // prologue barrier
   for (int e = 0; e <= m; ++e) {
     const bool has_cur = e < m;
@@ -1300,7 +1302,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                             const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
-  const XCtx X(c);
+  const XCtx X(c, G.cta);
   auto issue_tree = [&](int j) {  // lane 0: cache row, split column, record -> ring slot j % kRing
     const TreeHdr hd = G.hdr[j];
     unsigned long long *mb = &S.mbar[j % kRing];

@@ -169,7 +169,8 @@ class SamplerState:
     to the device before the next step, as tests/util.py:11-24 expects.
     """
 
-    def __init__(self, X, max_cuts, y, hp: Hyperparams, rng, sigma2: float, device: int = 0):
+    def __init__(self, X, max_cuts, y, hp: Hyperparams, rng, sigma2: float, device: int = 0,
+                 shard: tuple[int, int, int] | None = None):
         self.X = X
         self.max_cuts = max_cuts
         self.y = y
@@ -184,8 +185,15 @@ class SamplerState:
         self._h = C.c_void_p()
         seed = rng.seed if isinstance(rng, DeviceRNG) else 0
         d = N.dims(X.shape[0], X.shape[1], self._m, self._D)
-        N.check(N.lib().bart_create(d, N.hparams(hp, depth_probabilities(hp)), N.ptr(X), N.ptr(max_cuts),
-                                    N.ptr(y), float(sigma2), seed, self.device, C.byref(self._h)))
+        self.shard = shard  # (n_total, shard index, n_shards) for an n-sharded chain (paper_2410_23244_b200.shard)
+        if shard is None:
+            N.check(N.lib().bart_create(d, N.hparams(hp, depth_probabilities(hp)), N.ptr(X), N.ptr(max_cuts),
+                                        N.ptr(y), float(sigma2), seed, self.device, C.byref(self._h)))
+        else:
+            n_total, k, n_shards = shard
+            N.check(N.lib().bart_create_shard(d, int(n_total), int(k), int(n_shards),
+                                              N.hparams(hp, depth_probabilities(hp)), N.ptr(X), N.ptr(max_cuts),
+                                              N.ptr(y), float(sigma2), seed, self.device, C.byref(self._h)))
 
     # -- lifecycle
     def close(self) -> None:
@@ -357,6 +365,23 @@ class SamplerState:
         out = np.empty(Xq.shape[0], np.float64)
         N.check(N.lib().bart_predict_matrix(self._h, N.ptr(Xq), Xq.shape[0], N.ptr(out)))
         return out
+
+    # -- n-sharding (paper_2410_23244_b200.shard)
+    def shard_export(self) -> bytes:
+        buf = (C.c_uint8 * N.SHARD_HANDLE_BYTES)()
+        N.check(N.lib().bart_shard_export(self._h, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def shard_connect(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        if self.shard is None or len(handles) != self.shard[2] or len(blob) != len(handles) * N.SHARD_HANDLE_BYTES:
+            raise ValueError("need one exported handle per shard, in shard order")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        N.check(N.lib().bart_shard_connect(self._h, C.cast(buf, C.c_void_p)))
+
+    def set_copy_groups(self, groups: int) -> None:
+        """Test hook: emulate `groups` shards inside one launch on one device."""
+        N.check(N.lib().bart_set_copy_groups(self._h, int(groups)))
 
     def kernel_launches(self) -> int:
         return int(N.lib().bart_kernel_launches(self._h))

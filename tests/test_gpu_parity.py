@@ -221,3 +221,53 @@ def test_stream_mode_large_n_invariants():
     assert 0 < st.sigma2 < 10
     assert (f.cutpoint > 0).sum() > 0
     st.close()
+
+
+@pytest.mark.parametrize("groups", [2, 3, 8])
+def test_sharded_exchange_emulated(groups):
+    """n-sharding's exchange protocol (every shard adds into every shard's
+    words, each polls its own copy), emulated by splitting one
+    launch's CTAs into `groups` copy groups: decisions, counts and indices stay
+    bit-exact against the oracle."""
+    from paper_2410_23244_b200.dgp import friedman1
+    from paper_2410_23244_b200.grid import build_grid_uniform, quantize
+    from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
+    from paper_2410_23244_b200.sampler import StepRandoms, init_state, step
+    X, y, _ = friedman1(30011, 8, seed=11)
+    g = build_grid_uniform(X, 100)
+    Xq = quantize(X, g).data
+    hp, ys = derive_hyperparams(y, FitConfig(n_trees=30))
+    y32 = ys.forward(y).astype(np.float32)
+    st = init_state(Xq, g.counts, y32, hp, None)
+    st.set_copy_groups(groups)
+    st.enable_taps(True)
+    ora = OracleChain(Xq, g.counts, y32, hp)
+    rng = np.random.default_rng(groups)
+    for s in range(6):
+        rnd = StepRandoms.draw(rng, hp.n_trees, 1 << hp.max_depth, hp.nu + y.size)
+        taps = {}
+        ora.step(rnd.move_u, rnd.accept_u, rnd.leaf_z, rnd.chi2_value, taps)
+        step(st, hp, randoms=rnd)
+        counts, sums = st.taps()
+        np.testing.assert_array_equal(counts, taps["counts"])
+        np.testing.assert_allclose(sums, taps["sums"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_array_equal(st.last_accepted, ora.last_accepted, err_msg=f"step {s}")
+        np.testing.assert_array_equal(st.leaf_index, ora.leaf_index)
+        np.testing.assert_allclose(st.resid, ora.resid, rtol=1e-5, atol=1e-5)
+        assert st.sigma2 == pytest.approx(ora.sigma2, rel=1e-5)
+    st.close()
+
+
+def test_unconnected_shard_refuses_to_step():
+    from paper_2410_23244_b200.sampler import DeviceRNG, Hyperparams, SamplerState, step
+    rng = np.random.default_rng(0)
+    X = rng.integers(0, 9, (500, 3)).astype(np.uint8)
+    y = rng.normal(size=500).astype(np.float32)
+    hp = Hyperparams(leaf_sd=0.3, lam=0.1, n_trees=4, max_depth=4)
+    st = SamplerState(X, np.full(3, 8), y, hp, DeviceRNG(1), 1.0, 0, shard=(1000, 0, 2))
+    assert len(st.shard_export()) == 256
+    with pytest.raises(RuntimeError, match="not connected"):
+        step(st, hp)
+    with pytest.raises(ValueError):
+        st.shard_connect([st.shard_export()])  # one handle for two shards
+    st.close()
