@@ -118,6 +118,7 @@ int reset_mailbox_if_needed(bart_chain *, int64_t) {
   return BART_OK;
 }
 
+// One iteration: the propose kernel (injected or device randoms) + the sweep.
 int launch_iteration(bart_chain *h, int device_rng) {
   launch_propose(h->c, device_rng, h->stream);
   CUDA_TRY(cudaGetLastError());
@@ -833,6 +834,8 @@ int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
 }
 
 int bart_graph_active(bart_chain *h) { return h && h->graph ? 1 : 0; }
+
+
 
 int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
   if (!h || !ms) return fail(BART_EINVAL, "NULL argument");

@@ -213,7 +213,8 @@ class SamplerState:
 
     @property
     def n_points(self) -> int:
-        return self.y.size
+        """Points of the whole chain (all shards): the chi-square df is nu + n (sampler.py:259)."""
+        return self.shard[0] if self.shard is not None else self.y.size
 
     # -- lazily fetched host mirrors
     def _fetch(self, key):
