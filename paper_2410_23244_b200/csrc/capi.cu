@@ -118,12 +118,17 @@ int reset_mailbox_if_needed(bart_chain *, int64_t) {
   return BART_OK;
 }
 
-// One iteration: the propose kernel (injected or device randoms) + the sweep.
+// One iteration = ONE launch: the sweep kernel proposes every tree first
+// (injected or device randoms), then sweeps.
+ChainDev step_args(const bart_chain *h, int device_rng) {
+  ChainDev c = h->c;
+  c.propose_in_sweep = device_rng ? 1 : 2;
+  return c;
+}
+
 int launch_iteration(bart_chain *h, int device_rng) {
-  launch_propose(h->c, device_rng, h->stream);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
-  h->launches += 2;
+  CUDA_TRY((cudaError_t)sweep_launch(step_args(h, device_rng), h->smem, h->stream));
+  h->launches += 1;
   h->iteration += 1;
   return BART_OK;
 }
@@ -136,9 +141,8 @@ int ensure_graph(bart_chain *h) {
     cudaGetLastError();
     return BART_OK;
   }
-  launch_propose(h->c, 1, h->stream);
   cudaError_t e1 = cudaGetLastError();
-  cudaError_t e2 = (cudaError_t)sweep_launch(h->c, h->smem, h->stream);
+  cudaError_t e2 = (cudaError_t)sweep_launch(step_args(h, 1), h->smem, h->stream);
   cudaError_t e3 = cudaStreamEndCapture(h->stream, &g);
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || !g ||
       cudaGraphInstantiate(&h->graph, g, 0) != cudaSuccess) {
@@ -529,7 +533,7 @@ int bart_run(bart_chain *h, int64_t n_iter) {
   for (int64_t i = 0; i < n_iter; ++i) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
-      h->launches += 2;
+      h->launches += 1;
       h->iteration += 1;
     } else if (int rc = launch_iteration(h, 1)) {
       return rc;
@@ -818,7 +822,7 @@ int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
   for (int64_t i = 0; i < n_iter; ++i) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
-      h->launches += 2;
+      h->launches += 1;
       h->iteration += 1;
     } else if (int rc = launch_iteration(h, 1)) {
       return rc;
@@ -846,11 +850,10 @@ int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
   CUDA_TRY(cudaEventRecord(ev[0], h->stream));
   for (int64_t i = 0; i < n_iter; ++i) {
     CUDA_TRY(cudaEventRecord(ev[1 + 3 * i], h->stream));
-    launch_propose(h->c, 1, h->stream);
     CUDA_TRY(cudaEventRecord(ev[2 + 3 * i], h->stream));
-    CUDA_TRY((cudaError_t)sweep_launch(h->c, h->smem, h->stream));
+    CUDA_TRY((cudaError_t)sweep_launch(step_args(h, 1), h->smem, h->stream));
     CUDA_TRY(cudaEventRecord(ev[3 + 3 * i], h->stream));
-    h->launches += 2;
+    h->launches += 1;
     h->iteration += 1;
   }
   CUDA_TRY(cudaEventRecord(ev.back(), h->stream));

@@ -124,6 +124,7 @@ struct ChainDev {
   long long *trace;           // optional (m+1, nblk, 2) globaltimer: publish, gathered
   HP hp;
   int dbg;  // experiment switches (BART_DBG env var at create; 0 in production)
+  int propose_in_sweep;  // per launch: 0 proposals already made, 1 propose with device RNG, 2 with injected randoms
 };
 
 // ------------------------------------------------------------ Philox4x32-10

@@ -39,8 +39,11 @@
 // need resetting.  The same words extend to n-sharding across GPUs
 // (DESIGN.md §6): a shard adds into every shard's copy (c.xpeer) and polls
 // its own.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
+#include "propose.cuh"
 
 namespace bart {
 
@@ -1383,6 +1386,23 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   G.lenp = (uint32_t)((len + 15) & ~15);
   G.nwords = (int)(G.lenp >> 2);
 
+  if (c.propose_in_sweep) {
+    // phase 1 for every tree, spread over all warps of the grid (propose.cuh;
+    // sampler.py:469-526), then one grid barrier: the step is ONE launch.
+    // Scratch: the worker partials' buffer, unused until the first A pass.
+    const unsigned long long it = *c.iter_dev;
+    const int device_rng = c.propose_in_sweep == 1;
+    uint8_t *scratch = reinterpret_cast<uint8_t *>(&S.wsum[0][0]) + (size_t)warp * 512;
+    for (int j = G.cta + G.nblk * warp; j < c.m; j += G.nblk * kSweepWarps)
+      propose_tree(c, j, it, device_rng, scratch, reinterpret_cast<uint16_t *>(scratch + 128),
+                   reinterpret_cast<uint32_t *>(scratch + 384), lane);
+    if (device_rng && G.cta == G.nblk - 1 && warp == kSweepWarps - 1 && lane == 0) {
+      const uint2 key = make_uint2((uint32_t)c.seed, (uint32_t)(c.seed >> 32));
+      *c.rand_chi2 = chi2_draw(c.hp.nu + (double)c.n_total, it, key);
+    }
+    cooperative_groups::this_grid().sync();
+    asm volatile("fence.proxy.async;" ::: "memory");  // records written by generic stores, read by TMA
+  }
   for (int i = tid; i < c.m; i += kSweepThreads) G.hdr[i] = c.hdr[i];
   {  // exchange baselines: the words' values when the previous sweep ended
     unsigned long long *dst = &S.xprev[0][0];
