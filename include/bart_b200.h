@@ -141,6 +141,30 @@ int bart_get_timeline(bart_chain *h, int64_t *out);
  * exchange of the last sweep: (m+1, ctas, 2). */
 int bart_get_trace(bart_chain *h, int64_t *out);
 
+/* ---- fit() trace kept on the device (regression.fit's chain loop, regression.py:183-201) ----
+ * Instead of reading last_accepted / sigma2 / predictions back after every
+ * iteration, the sweep writes each iteration's accept flags and sigma2 into
+ * device history rows, and bart_trace_keep records a kept draw
+ * asynchronously: per-point running mean/variance of the training-row sum of
+ * trees (Welford, f64), optionally the whole draw, the draw at the first
+ * BART_TRACE_POINTS rows (cross-chain diagnostics), test-row predictions,
+ * sigma2, mean leaves per tree, and the forest.  One read at the end. */
+#define BART_TRACE_POINTS 8
+typedef struct {
+  int64_t n_iter, n_keep, n_test;  /* capacities; n_test rows of X_test */
+  int32_t store_train_draws, store_forests;
+} bart_trace_opts;
+int bart_trace_begin(bart_chain *h, const bart_trace_opts *opts, const uint8_t *X_test /* (n_test, p) or NULL */);
+int bart_trace_keep(bart_chain *h);
+int bart_trace_counts(bart_chain *h, int64_t *n_iter, int64_t *n_keep);
+/* any pointer may be NULL; shapes: accepted (n_iter, m), sigma2_iter (n_iter), sigma2_keep (n_keep),
+ * train_mean/var (n), train_draws (n_keep, n), train_points (n_keep, min(n, 8)), test_draws (n_keep, n_test),
+ * mean_leaves (n_keep), axis/cutpoint (n_keep, m, 2^(D-1)), leaf_value (n_keep, m, 2^D) */
+int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, double *sigma2_keep, double *train_mean,
+                    double *train_var, double *train_draws, double *train_points, double *test_draws,
+                    double *mean_leaves, uint16_t *axis, uint8_t *cutpoint, float *leaf_value);
+int bart_trace_end(bart_chain *h);
+
 /* ---- predictions (trees.sum_leaf_values / evaluate_forest, trees.py:206-223) ---- */
 /* sum of trees from the cached leaf index, f64 in tree order: (n,) */
 int bart_predict_cached(bart_chain *h, double *out);

@@ -33,6 +33,14 @@ class HParams(C.Structure):
     ]
 
 
+class TraceOpts(C.Structure):
+    _fields_ = [("n_iter", C.c_int64), ("n_keep", C.c_int64), ("n_test", C.c_int64),
+                ("store_train_draws", C.c_int32), ("store_forests", C.c_int32)]
+
+
+TRACE_POINTS = 8
+
+
 class Randoms(C.Structure):
     _fields_ = [("move_u", C.c_void_p), ("accept_u", C.c_void_p), ("leaf_z", C.c_void_p), ("chi2", C.c_double)]
 
@@ -46,6 +54,11 @@ _SIGS = {
     "bart_shard_export": [_P, _P],
     "bart_shard_connect": [_P, _P],
     "bart_set_copy_groups": [_P, C.c_int],
+    "bart_trace_begin": [_P, C.POINTER(TraceOpts), _P],
+    "bart_trace_keep": [_P],
+    "bart_trace_counts": [_P, _P, _P],
+    "bart_trace_read": [_P] + [_P] * 12,
+    "bart_trace_end": [_P],
     "bart_set_state": [_P, _P, _P, _P, _P, _P, C.c_double],
     "bart_set_hparams": [_P, C.POINTER(HParams)],
     "bart_set_sigma2": [_P, C.c_double],

@@ -73,6 +73,18 @@ HP to_hp(const bart_hparams *h) {
 
 }  // namespace
 
+struct TraceState {  // fit() trace kept on the device (bart_trace_begin)
+  bool on = false;
+  int64_t iter_cap = 0, keep_cap = 0, n_test = 0, ld_test = 0, iter0 = 0, kept = 0;
+  int store_train = 0, store_forests = 0, npts = 0;
+  uint8_t *acc = nullptr, *Xt_test = nullptr, *f_cut = nullptr;
+  uint16_t *f_axis = nullptr;
+  float *f_leaf = nullptr;
+  double *sig_iter = nullptr, *sig_keep = nullptr, *mean = nullptr, *m2 = nullptr, *train = nullptr, *pts = nullptr,
+         *test = nullptr, *mleaves = nullptr;
+  std::vector<void *> bufs;
+};
+
 struct bart_chain {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -88,6 +100,7 @@ struct bart_chain {
   std::vector<void *> owned;
   std::vector<void *> ipc_opened;  // peer shards' exchange buffers (cudaIpcOpenMemHandle)
   bool shard_pending = false;      // created as a shard, not yet connected
+  TraceState tr;
 };
 
 namespace {
@@ -96,6 +109,7 @@ void free_chain(bart_chain *h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (void *p : h->tr.bufs) cudaFree(p);
   for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : h->owned)
     if (p) cudaFree(p);
@@ -154,6 +168,30 @@ int ensure_graph(bart_chain *h) {
   return BART_OK;
 }
 
+}  // namespace
+
+// ---- fit() trace on the device ----
+namespace {
+void trace_free(bart_chain *h) {
+  for (void *p : h->tr.bufs) cudaFree(p);
+  h->tr = TraceState{};
+  h->c.acc_hist = nullptr;
+  h->c.sig_hist = nullptr;
+  h->c.hist_cap = 0;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+}
+template <typename T>
+cudaError_t trace_alloc(bart_chain *h, T **p, size_t count) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+  if (e == cudaSuccess) {
+    h->tr.bufs.push_back(*p);
+    e = cudaMemsetAsync(*p, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16, h->stream);
+  }
+  return e;
+}
 }  // namespace
 
 extern "C" {
@@ -435,6 +473,134 @@ int bart_set_copy_groups(bart_chain *h, int groups) {
   return BART_OK;
 }
 
+
+int bart_trace_begin(bart_chain *h, const bart_trace_opts *o, const uint8_t *X_test) {
+  if (!h || !o) return fail(BART_EINVAL, "NULL argument");
+  if (o->n_iter < 0 || o->n_keep < 0 || o->n_test < 0 || (o->n_test > 0 && !X_test))
+    return fail(BART_EINVAL, "bad trace options");
+  CUDA_TRY(cudaSetDevice(h->device));
+  trace_free(h);
+  ChainDev &c = h->c;
+  TraceState &t = h->tr;
+  t.iter_cap = o->n_iter;
+  t.keep_cap = o->n_keep;
+  t.n_test = o->n_test;
+  t.ld_test = round16(o->n_test);
+  t.store_train = o->store_train_draws;
+  t.store_forests = o->store_forests;
+  t.npts = (int)(c.n < BART_TRACE_POINTS ? c.n : BART_TRACE_POINTS);
+  t.iter0 = h->iteration;
+  const size_t K = (size_t)t.keep_cap, n = (size_t)c.n;
+  CUDA_TRY(trace_alloc(h, &t.acc, (size_t)t.iter_cap * c.m));
+  CUDA_TRY(trace_alloc(h, &t.sig_iter, (size_t)t.iter_cap));
+  CUDA_TRY(trace_alloc(h, &t.sig_keep, K));
+  CUDA_TRY(trace_alloc(h, &t.mean, n));
+  CUDA_TRY(trace_alloc(h, &t.m2, n));
+  CUDA_TRY(trace_alloc(h, &t.pts, K * t.npts));
+  CUDA_TRY(trace_alloc(h, &t.mleaves, K));
+  if (t.store_train) CUDA_TRY(trace_alloc(h, &t.train, K * n));
+  if (t.n_test) {
+    CUDA_TRY(trace_alloc(h, &t.test, K * (size_t)t.n_test));
+    CUDA_TRY(trace_alloc(h, &t.Xt_test, (size_t)t.ld_test * c.p));
+    DevBuf xs;
+    CUDA_TRY(xs.alloc((size_t)t.n_test * c.p));
+    CUDA_TRY(cudaMemcpyAsync(xs.p, X_test, (size_t)t.n_test * c.p, cudaMemcpyHostToDevice, h->stream));
+    launch_transpose_u8(xs.as<uint8_t>(), t.n_test, c.p, c.p, t.Xt_test, t.ld_test, h->stream);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  if (t.store_forests) {
+    CUDA_TRY(trace_alloc(h, &t.f_axis, K * c.m * c.half));
+    CUDA_TRY(trace_alloc(h, &t.f_cut, K * c.m * c.half));
+    CUDA_TRY(trace_alloc(h, &t.f_leaf, K * c.m * c.size));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  c.acc_hist = t.acc;
+  c.sig_hist = t.sig_iter;
+  c.hist_base = h->iteration;
+  c.hist_cap = t.iter_cap;
+  t.on = true;
+  if (h->graph) {  // the captured launch carries the trace pointers
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return BART_OK;
+}
+
+int bart_trace_keep(bart_chain *h) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  TraceState &t = h->tr;
+  if (!t.on) return fail(BART_ESTATE, "no trace (bart_trace_begin)");
+  if (t.kept >= t.keep_cap) return fail(BART_EINVAL, "trace full: n_keep draws already kept");
+  CUDA_TRY(cudaSetDevice(h->device));
+  ChainDev &c = h->c;
+  cudaStream_t s = h->stream;
+  const size_t k = (size_t)t.kept;
+  launch_trace_train(c.L, c.n, c.n_pad, c.m, c.size, c.leaf, t.kept + 1, t.mean, t.m2,
+                     t.store_train ? t.train + k * c.n : nullptr, t.pts + k * t.npts, t.npts, s);
+  if (t.n_test)
+    launch_evaluate(t.Xt_test, t.n_test, t.ld_test, c.D, c.half, c.m, c.axis, c.cut, c.leaf, t.test + k * t.n_test, s);
+  launch_mean_leaves(c.cut, c.m, c.half, t.mleaves + k, s);
+  h->launches += t.n_test ? 3 : 2;
+  CUDA_TRY(cudaMemcpyAsync(t.sig_keep + k, c.sigma2, 8, cudaMemcpyDeviceToDevice, s));
+  if (t.store_forests) {
+    CUDA_TRY(cudaMemcpyAsync(t.f_axis + k * c.m * c.half, c.axis, (size_t)c.m * c.half * 2, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(t.f_cut + k * c.m * c.half, c.cut, (size_t)c.m * c.half, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(t.f_leaf + k * c.m * c.size, c.leaf, (size_t)c.m * c.size * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_TRY(cudaGetLastError());
+  t.kept += 1;
+  return BART_OK;
+}
+
+int bart_trace_counts(bart_chain *h, int64_t *n_iter, int64_t *n_keep) {
+  if (!h || !n_iter || !n_keep) return fail(BART_EINVAL, "NULL argument");
+  const TraceState &t = h->tr;
+  if (!t.on) return fail(BART_ESTATE, "no trace (bart_trace_begin)");
+  const int64_t it = h->iteration - t.iter0;
+  *n_iter = it < t.iter_cap ? it : t.iter_cap;
+  *n_keep = t.kept;
+  return BART_OK;
+}
+
+int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, double *sigma2_keep, double *train_mean,
+                    double *train_var, double *train_draws, double *train_points, double *test_draws,
+                    double *mean_leaves, uint16_t *axis, uint8_t *cutpoint, float *leaf_value) {
+  int64_t ni = 0, nk = 0;
+  if (int rc = bart_trace_counts(h, &ni, &nk)) return rc;
+  if (int rc = bart_sync(h)) return rc;
+  const TraceState &t = h->tr;
+  const ChainDev &c = h->c;
+  auto d2h = [](void *dst, const void *src, size_t bytes) {
+    return dst && bytes ? cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) : cudaSuccess;
+  };
+  CUDA_TRY(d2h(accepted, t.acc, (size_t)ni * c.m));
+  CUDA_TRY(d2h(sigma2_iter, t.sig_iter, (size_t)ni * 8));
+  CUDA_TRY(d2h(sigma2_keep, t.sig_keep, (size_t)nk * 8));
+  CUDA_TRY(d2h(train_mean, t.mean, (size_t)c.n * 8));
+  if (train_var) {  // sample variance over the kept draws
+    CUDA_TRY(d2h(train_var, t.m2, (size_t)c.n * 8));
+    for (int64_t i = 0; i < c.n; ++i) train_var[i] = nk > 1 ? train_var[i] / (double)(nk - 1) : 0.0;
+  }
+  if (t.store_train) CUDA_TRY(d2h(train_draws, t.train, (size_t)nk * c.n * 8));
+  CUDA_TRY(d2h(train_points, t.pts, (size_t)nk * t.npts * 8));
+  if (t.n_test) CUDA_TRY(d2h(test_draws, t.test, (size_t)nk * t.n_test * 8));
+  CUDA_TRY(d2h(mean_leaves, t.mleaves, (size_t)nk * 8));
+  if (t.store_forests) {
+    CUDA_TRY(d2h(axis, t.f_axis, (size_t)nk * c.m * c.half * 2));
+    CUDA_TRY(d2h(cutpoint, t.f_cut, (size_t)nk * c.m * c.half));
+    CUDA_TRY(d2h(leaf_value, t.f_leaf, (size_t)nk * c.m * c.size * 4));
+  }
+  return BART_OK;
+}
+
+int bart_trace_end(bart_chain *h) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  trace_free(h);
+  return BART_OK;
+}
+
 int bart_destroy(bart_chain *h) {
   free_chain(h);
   return BART_OK;
@@ -505,8 +671,8 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
     CUDA_TRY(cudaMemcpyAsync(c.rand_acc, rnd->accept_u, (size_t)c.m * 8, cudaMemcpyHostToDevice, h->stream));
     CUDA_TRY(cudaMemcpyAsync(c.rand_z, rnd->leaf_z, (size_t)c.m * c.size * 8, cudaMemcpyHostToDevice, h->stream));
     CUDA_TRY(cudaMemcpyAsync(c.rand_chi2, &rnd->chi2, 8, cudaMemcpyHostToDevice, h->stream));
+    // (pageable sources: the copies are staged before cudaMemcpyAsync returns)
     if (int rc = launch_iteration(h, 0)) return rc;
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
   } else {
     if (int rc = launch_iteration(h, 1)) return rc;
   }

@@ -125,6 +125,11 @@ struct ChainDev {
   HP hp;
   int dbg;  // experiment switches (BART_DBG env var at create; 0 in production)
   int propose_in_sweep;  // per launch: 0 proposals already made, 1 propose with device RNG, 2 with injected randoms
+  // on-device trace (bart_trace_begin): per-iteration accept flags and sigma2,
+  // rows [iter - hist_base] of (hist_cap, m) / (hist_cap)
+  uint8_t *acc_hist;
+  double *sig_hist;
+  int64_t hist_base, hist_cap;
 };
 
 // ------------------------------------------------------------ Philox4x32-10

@@ -171,3 +171,63 @@ void launch_resid(const float *y, const double *pred, float *r, int64_t n, cudaS
 }
 
 }  // namespace bart
+
+namespace bart {
+
+// fit() trace, one kept draw (regression.py:191-200): the sum of trees at the
+// training rows from the cached leaf index (f64, tree order, as sum_leaf_values,
+// trees.py:206-218), folded into per-point running moments (Welford, draw
+// number k >= 1), optionally stored whole and at the first npts rows.
+__global__ void trace_train_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m, int size,
+                                   const float *__restrict__ leaf, double k, double *__restrict__ mean,
+                                   double *__restrict__ m2, double *__restrict__ draw, double *__restrict__ pts,
+                                   int npts) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w * 4 >= ld) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int j = 0; j < m; ++j) {
+    const uint32_t l = reinterpret_cast<const uint32_t *>(L + (size_t)j * ld)[w];
+    const float *row = leaf + (size_t)j * size;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int64_t i = w * 4 + b;
+    if (i >= n) break;
+    const double x = acc[b], mu = mean[i], d = x - mu, mu2 = mu + d / k;
+    mean[i] = mu2;
+    m2[i] += d * (x - mu2);
+    if (draw) draw[i] = x;
+    if (i < npts) pts[i] = x;
+  }
+}
+
+// leaves per tree, averaged: every nonzero cutpoint is an internal node of a
+// valid heap tree, and a binary tree has one more leaf than internal nodes
+__global__ void mean_leaves_kernel(const uint8_t *__restrict__ cut, int m, int half, double *__restrict__ out) {
+  __shared__ int part[32];
+  int cnt = 0;
+  for (int i = threadIdx.x; i < m * half; i += blockDim.x) cnt += cut[i] != 0;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += part[k];
+    *out = (double)(t + m) / (double)m;
+  }
+}
+
+void launch_trace_train(const uint8_t *L, int64_t n, int64_t ld, int m, int size, const float *leaf, int64_t k,
+                        double *mean, double *m2, double *draw, double *pts, int npts, cudaStream_t s) {
+  const int64_t words = ld / 4;
+  trace_train_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(L, n, ld, m, size, leaf, (double)k, mean, m2,
+                                                                     draw, pts, npts);
+}
+
+void launch_mean_leaves(const uint8_t *cut, int m, int half, double *out, cudaStream_t s) {
+  mean_leaves_kernel<<<1, 1024, 0, s>>>(cut, m, half, out);
+}
+
+}  // namespace bart

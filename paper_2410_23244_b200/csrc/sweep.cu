@@ -895,7 +895,7 @@ __device__ __forceinline__ void decide_fast(SweepSmem &S, Dec &Do, const DecIn &
 // 836-848, 868-870) and the parity taps.
 __device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, const Prep &P, const Dec &Di,
                                             const uint8_t *rec, const TreeHdr hd, int e, int lane,
-                                            const DecConst &K) {
+                                            const DecConst &K, int64_t hist_row) {
   const TreeMove &mv = rec_hdr(rec);
   const double *z = rec_z(rec, c.size);
   const int size = c.size, half = c.half;
@@ -906,6 +906,7 @@ __device__ __forceinline__ void decide_post(const ChainDev &c, SweepSmem &S, con
   const float v_par = __double2float_rn(Di.v_s[ns]);
   if (lane == 0) {
     c.accepted[e] = (uint8_t)acc;
+    if (hist_row >= 0) c.acc_hist[hist_row * c.m + e] = (uint8_t)acc;  // fit() trace (regression.py:190)
     if (acc) {
       c.axis[(size_t)e * half + t] = grow ? hd.axis : (uint16_t)0;
       c.cut[(size_t)e * half + t] = grow ? hd.cut : (uint8_t)0;
@@ -1306,6 +1307,9 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
                                             const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
   const XCtx X(c, G.cta);
+  // trace row of this iteration (read before the sigma CTA bumps the counter)
+  const int64_t hrow = c.acc_hist ? (int64_t)*c.iter_dev - c.hist_base : -1;
+  const int64_t hist_row = (hrow >= 0 && hrow < c.hist_cap) ? hrow : -1;
   auto issue_tree = [&](int j) {  // lane 0: cache row, split column, record -> ring slot j % kRing
     const TreeHdr hd = G.hdr[j];
     unsigned long long *mb = &S.mbar[j % kRing];
@@ -1347,12 +1351,14 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     if (e + 1 < m) prepare_tree(e + 1);
     TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 13] = gtimer();
     mbar_wait(&S.dec_mbar[e & 1], par2(e));  // exchange e done, decision e taken
-    if (e < m && G.cta == e % G.nblk) decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K);
+    if (e < m && G.cta == e % G.nblk)
+      decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K, hist_row);
     if (e == m && G.cta == m % G.nblk && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
       const HP &hp = c.hp;
       const double s2 = __ddiv_rn(__dadd_rn(__dmul_rn(hp.nu, hp.lam), S.tot_sum[0]), *c.rand_chi2);
       *c.sigma2_draw = s2;
       if (hp.update_sigma) *c.sigma2 = s2;
+      if (hist_row >= 0) c.sig_hist[hist_row] = hp.update_sigma ? s2 : *c.sigma2;
       *c.iter_dev += 1ull;
     }
     if (e == m && G.cta == 0) {  // the next sweep's exchange baselines

@@ -380,6 +380,44 @@ class SamplerState:
         buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
         N.check(N.lib().bart_shard_connect(self._h, C.cast(buf, C.c_void_p)))
 
+    # -- fit() trace kept on the device (bart_trace_*)
+    def trace_begin(self, n_iter: int, n_keep: int, Xq_test: np.ndarray | None = None,
+                    store_train_draws: bool = False, store_forests: bool = False) -> None:
+        X = None if Xq_test is None else np.ascontiguousarray(Xq_test, np.uint8)
+        opts = N.TraceOpts(int(n_iter), int(n_keep), 0 if X is None else int(X.shape[0]),
+                           int(bool(store_train_draws)), int(bool(store_forests)))
+        N.check(N.lib().bart_trace_begin(self._h, C.byref(opts), N.ptr(X)))
+        self._trace = dict(n_test=opts.n_test, store_train=bool(store_train_draws), store_forests=bool(store_forests))
+
+    def trace_keep(self) -> None:
+        """Record the current state as a kept draw (asynchronous)."""
+        N.check(N.lib().bart_trace_keep(self._h))
+
+    def trace_read(self) -> dict:
+        """Everything recorded since trace_begin, in the reference's layouts (scaled units)."""
+        ni, nk = C.c_int64(), C.c_int64()
+        N.check(N.lib().bart_trace_counts(self._h, C.byref(ni), C.byref(nk)))
+        ni, nk, n, m, D = ni.value, nk.value, self.y.size, self._m, self._D
+        o = self._trace
+        out = dict(
+            accepted=np.empty((ni, m), np.uint8), sigma2_iter=np.empty(ni), sigma2_keep=np.empty(nk),
+            train_mean=np.empty(n), train_var=np.empty(n),
+            train_draws=np.empty((nk, n)) if o["store_train"] else None,
+            train_points=np.empty((nk, min(n, N.TRACE_POINTS))),
+            test_draws=np.empty((nk, o["n_test"])) if o["n_test"] else None,
+            mean_leaves=np.empty(nk),
+            axis=np.empty((nk, m, split_slots(D)), np.uint16) if o["store_forests"] else None,
+            cutpoint=np.empty((nk, m, split_slots(D)), np.uint8) if o["store_forests"] else None,
+            leaf_value=np.empty((nk, m, heap_size(D)), np.float32) if o["store_forests"] else None)
+        keys = ["accepted", "sigma2_iter", "sigma2_keep", "train_mean", "train_var", "train_draws", "train_points",
+                "test_draws", "mean_leaves", "axis", "cutpoint", "leaf_value"]
+        N.check(N.lib().bart_trace_read(self._h, *[N.ptr(out[k]) for k in keys]))
+        out["accepted"] = out["accepted"].astype(bool)
+        return out
+
+    def trace_end(self) -> None:
+        N.check(N.lib().bart_trace_end(self._h))
+
     def set_copy_groups(self, groups: int) -> None:
         """Test hook: emulate `groups` shards inside one launch on one device."""
         N.check(N.lib().bart_set_copy_groups(self._h, int(groups)))
