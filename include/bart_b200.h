@@ -198,6 +198,16 @@ int64_t bart_kernel_launches(bart_chain *h);
 int bart_graph_active(bart_chain *h);
 int bart_sweep_config(bart_chain *h, int32_t *out /* [ctas, threads, chunk, smem_bytes, stream] */);
 
+/* ---- binning (bforge/grid.py) ----
+ * column min / max of the raw (n, p) row-major f64 matrix (the span of
+ * build_grid_uniform, grid.py:77-95; EINVAL on non-finite values), and
+ * quantize (grid.py:121-134): out[i, a] = #{cutpoints of axis a <= X[i, a]}
+ * (np.searchsorted side="right"), cutpoints of axis a at
+ * cutpoints[offsets[a] .. offsets[a+1]), <= 255 per axis. */
+int bart_grid_minmax(const double *X, int64_t n, int32_t p, double *lo, double *hi, int device);
+int bart_quantize(const double *X, int64_t n, int32_t p, const double *cutpoints, const int64_t *offsets,
+                  uint8_t *out, int device);
+
 const char *bart_last_error(void);
 const char *bart_version(void);
 

@@ -14,8 +14,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libbart_b200.so")
-SOURCES = ["propose.cu", "sweep.cu", "forest.cu", "capi.cu"]
-HEADERS = ["common.cuh", "internal.h"]
+SOURCES = ["propose.cu", "sweep.cu", "forest.cu", "binning.cu", "capi.cu"]
+HEADERS = ["common.cuh", "internal.h", "propose.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

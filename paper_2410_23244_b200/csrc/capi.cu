@@ -601,6 +601,50 @@ int bart_trace_end(bart_chain *h) {
   return BART_OK;
 }
 
+// ---- binning (grid.py) ----
+int bart_grid_minmax(const double *X, int64_t n, int32_t p, double *lo, double *hi, int device) {
+  if (!X || !lo || !hi || n < 1 || p < 1) return fail(BART_EINVAL, "bad minmax arguments");
+  CUDA_TRY(cudaSetDevice(device));
+  DevBuf dx, keys, bad, dlo, dhi;
+  CUDA_TRY(dx.alloc((size_t)n * p * 8));
+  CUDA_TRY(keys.alloc((size_t)2 * p * 8));
+  CUDA_TRY(bad.alloc(8));
+  CUDA_TRY(dlo.alloc((size_t)p * 8));
+  CUDA_TRY(dhi.alloc((size_t)p * 8));
+  CUDA_TRY(cudaMemcpy(dx.p, X, (size_t)n * p * 8, cudaMemcpyHostToDevice));
+  launch_minmax(dx.as<double>(), n, p, keys.as<long long>(), bad.as<unsigned long long>(), dlo.as<double>(),
+                dhi.as<double>(), 0);
+  unsigned long long nbad = 0;
+  CUDA_TRY(cudaMemcpy(&nbad, bad.p, 8, cudaMemcpyDeviceToHost));
+  if (nbad) return fail(BART_EINVAL, "predictors must be finite (" + std::to_string(nbad) + " non-finite values)");
+  CUDA_TRY(cudaMemcpy(lo, dlo.p, (size_t)p * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hi, dhi.p, (size_t)p * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_quantize(const double *X, int64_t n, int32_t p, const double *cutpoints, const int64_t *offsets,
+                  uint8_t *out, int device) {
+  if (!X || !cutpoints || !offsets || !out || n < 0 || p < 1) return fail(BART_EINVAL, "bad quantize arguments");
+  for (int a = 0; a < p; ++a)
+    if (offsets[a + 1] < offsets[a] || offsets[a + 1] - offsets[a] > 255)
+      return fail(BART_EINVAL, "each axis needs 0..255 cutpoints (grid.py:18)");
+  if (n == 0) return BART_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t nc = offsets[p];
+  DevBuf dx, dc, doff, dout;
+  CUDA_TRY(dx.alloc((size_t)n * p * 8));
+  CUDA_TRY(dc.alloc((size_t)(nc > 0 ? nc : 1) * 8));
+  CUDA_TRY(doff.alloc((size_t)(p + 1) * 8));
+  CUDA_TRY(dout.alloc((size_t)n * p));
+  CUDA_TRY(cudaMemcpy(dx.p, X, (size_t)n * p * 8, cudaMemcpyHostToDevice));
+  if (nc > 0) CUDA_TRY(cudaMemcpy(dc.p, cutpoints, (size_t)nc * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(doff.p, offsets, (size_t)(p + 1) * 8, cudaMemcpyHostToDevice));
+  launch_quantize(dx.as<double>(), n, p, dc.as<double>(), doff.as<int64_t>(), dout.as<uint8_t>(), 0);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, dout.p, (size_t)n * p, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
 int bart_destroy(bart_chain *h) {
   free_chain(h);
   return BART_OK;

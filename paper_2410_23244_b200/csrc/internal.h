@@ -29,5 +29,9 @@ void launch_resid(const float *y, const double *pred, float *r, int64_t n, cudaS
 void launch_trace_train(const uint8_t *L, int64_t n, int64_t ld, int m, int size, const float *leaf, int64_t k,
                         double *mean, double *m2, double *draw, double *pts, int npts, cudaStream_t s);
 void launch_mean_leaves(const uint8_t *cut, int m, int half, double *out, cudaStream_t s);
+void launch_minmax(const double *X, int64_t n, int p, long long *keys, unsigned long long *bad, double *lo, double *hi,
+                   cudaStream_t s);
+void launch_quantize(const double *X, int64_t n, int p, const double *cuts, const int64_t *off, uint8_t *out,
+                     cudaStream_t s);
 
 }  // namespace bart

@@ -1,0 +1,38 @@
+"""GPU binning (csrc/binning.cu) against the reference's numpy semantics
+(grid.py:77-95 uniform grid, grid.py:121-134 searchsorted side="right")."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_quantize_matches_numpy_with_ties_and_edges():
+    from paper_2410_23244_b200.grid import build_grid_midpoints, build_grid_uniform, quantize
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(20011, 7)) * 10.0 ** rng.integers(-3, 4, size=7)
+    X[:, 3] = np.round(X[:, 3])              # many ties
+    X[:, 5] = 2.5                            # constant axis: no cutpoints
+    X[:100, 0] = X[:100, 0].max()            # values equal to the top of the range
+    for grid in (build_grid_uniform(X, 100), build_grid_uniform(X, 255), build_grid_midpoints(X)):
+        want = quantize(X, grid).data
+        got = quantize(X, grid, device=0).data
+        np.testing.assert_array_equal(got, want)
+        # exact cutpoint values go right (ties right, grid.py:127-128)
+        cuts = grid.cutpoints[0]
+        probe = np.tile(cuts[:, None], (1, 7))
+        np.testing.assert_array_equal(quantize(probe, grid, device=0).data[:, 0], np.arange(1, cuts.size + 1))
+
+
+def test_uniform_grid_ranges_on_device():
+    from paper_2410_23244_b200.grid import build_grid_uniform
+    rng = np.random.default_rng(1)
+    X = rng.normal(size=(100003, 11))
+    X[:, 2] = -np.abs(X[:, 2])               # all negative
+    X[:, 4] = 0.0                            # constant
+    a, b = build_grid_uniform(X, 100), build_grid_uniform(X, 100, device=0)
+    for ca, cb in zip(a.cutpoints, b.cutpoints):
+        np.testing.assert_array_equal(ca, cb)
+    with pytest.raises(ValueError):
+        X[7, 1] = np.nan
+        build_grid_uniform(X, 100, device=0)
