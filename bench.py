@@ -256,12 +256,16 @@ def run_ours(args):
     value = (1 if sharded else world) * args.steps / t_max
 
     # per-kernel durations (events around each launch, not graph-replayed)
+    # The step is ONE kernel launch (sweep_kernel: in-kernel proposals, the
+    # sequential tree sweep, sigma), so its average launch duration is the
+    # timed region's per-step time on this rank (CUDA events, graph replay).
+    # Events around individual non-graph launches are reported beside it.
     prof = np.zeros(3, np.float32)
     kp = max(10, min(args.steps, 50))
     N.check(N.lib().bart_profile(st.handle, kp, N.ptr(prof)))
     st._after_step(kp)
-    sweep_ms = float(prof[1]) / kp
-    propose_ms = float(prof[2]) / kp
+    sweep_ms = float(ms[0]) / args.steps
+    single_launch_ms = float(prof[1]) / kp
     alg_bytes = 10.0 * args.n * args.m
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
@@ -304,8 +308,14 @@ def run_ours(args):
                             "D2H last_accepted/sigma2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": committed_traffic(),
-                         "kernel": "sweep_kernel", "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_ms": sweep_ms, "propose_ms": propose_ms, "peak_source": peak_src},
+                         "kernel": "sweep_kernel (the whole step: one launch per iteration)",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "algorithmic_bytes_formula": "10*n*ntree: per point and tree 1 B leaf index + 1 B X "
+                                                      "column + 2x4 B residual (SURVEY.md 8d)",
+                         "kernel_ms": sweep_ms, "kernel_ms_single_launch_events": single_launch_ms,
+                         "peak_source": peak_src,
+                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                           "profiles/sweep_ncu_summary.json"},
             "cpu_baseline": cpu,
             "gpu_launches": gpu_launches,
             "cuda_graph": graph,
