@@ -58,8 +58,11 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
 TIMELINE_LIB = os.path.join(PKG, "lib", "libbart_b200_timeline.so")
 
 
-def build_timeline() -> str:
+def build_timeline(defines: tuple = ()) -> str:
     """The instrumented variant tools/timeline.py loads (per-phase clock stamps)."""
+    if defines:
+        tag = "_".join(d.replace("=", "") for d in defines)
+        return build(out=TIMELINE_LIB.replace(".so", f"_{tag}.so"), defines=("BART_TIMELINE=1", *defines))
     return build(out=TIMELINE_LIB, defines=("BART_TIMELINE=1",))
 
 

@@ -293,7 +293,7 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   OWN(s2d, 1);
   OWN(acc, (size_t)c.m);
   OWN(xacc, (size_t)kXSets * kXSetWords);
-  OWN(xsnap, 1 + (size_t)kXSets * kXSetWords);
+  OWN(xsnap, 1 + (size_t)kXSets * kXPrevWords);
   OWN(errf, 32);
   OWN(cacc, (size_t)kCSets * kCSetWords);
   OWN(csnap, (size_t)kCSets * kCSetWords);

@@ -26,13 +26,15 @@ constexpr int kMaxCtas = 256;         // CTAs per shard (one per SM)
 constexpr int kProposeWarps = 4;
 constexpr int kMaxShards = 8;         // n-shards whose exchange words a sweep adds into
 // Exchange accumulators: kXSets sets (exchange X uses set X % kXSets), each
-// kSlotsMax+1 slot sectors of kXSlotWords u64 (32 B): 3 fixed-point limbs of
-// the slot's f64 residual sum + one unused word.  One warp instruction adds
-// (and polls) 8 slots: lane 4s+q owns word q of slot s, so the L2 sees one
-// coalesced 32-B atomic per slot per CTA.
+// kSlotsMax+1 slots of 3 tagged fixed-point limbs of the slot's f64 residual
+// sum.  Slots sit kXSlotWords (256 B) apart, so the slots of one exchange
+// hit different L2 lines and slices: same-line atomics from 148 CTAs
+// serialise (tools/xbench2.cu; +2.4% end to end over 32-B slots).  One warp
+// instruction adds (and polls) 8 slots: lane 4s+q owns word q of slot s.
 constexpr int kXSets = 3;
-constexpr int kXSlotWords = 4;
+constexpr int kXSlotWords = 32;
 constexpr size_t kXSetWords = (size_t)(kSlotsMax + 1) * kXSlotWords;
+constexpr size_t kXPrevWords = (size_t)(kSlotsMax + 1) * 4;  // per set: baselines of the used words (s*4+q)
 // Count channel: the per-leaf point counts of tree j (needed one exchange
 // before tree j's decision) travel through their own tagged words, set j % 4,
 // one u64 per slot, added and polled by the helper warps.
@@ -110,7 +112,7 @@ struct ChainDev {
                                 // when one launch emulates several shards on one device)
   int64_t n_total;              // points of the whole chain (chi-square df, sampler.py:259)
   int *err;                     // device error flags (bit 0: exchange value out of fixed-point range)
-  unsigned long long *xsnap;    // [1 + kXSets*(kSlotsMax+1)*4]: exchange count, then every polled
+  unsigned long long *xsnap;    // [1 + kXSets*kXPrevWords]: exchange count, then every polled
                                 // word's last complete value (the next sweep's baseline)
   unsigned long long *cacc;     // this shard's count channel [kCSets][kCSetWords] (polled)
   unsigned long long *cpeer[kMaxShards];  // every shard's cacc

@@ -91,7 +91,7 @@ struct __align__(16) SweepSmem {
   double q_s[kSlotsMax + 1];                // posterior means (control scratch, wide trees)
   float row[256];                           // new leaf row (helper scratch)
   float dlt[256];                           // residual delta by larger-tree heap index
-  unsigned long long xprev[kXSets][kXSetWords];       // last complete value of every exchange word
+  unsigned long long xprev[kXSets][kXPrevWords];      // last complete value of every exchange word (s*4+q)
   unsigned long long cprev[kCSets][kCSetWords];       // last complete value of every count word
   unsigned long long mbar[kRing];      // TMA ring slot filled (per tree j % kRing)
   unsigned long long cnt_mbar[2];     // workers -> helper: B pass counts of tree t in wcnt[t & 1]
@@ -552,12 +552,12 @@ __device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns,
       const int s = 8 * (k0 + k) + (lane >> 2);
       w[k] = 0ull;
       if (s < ns && q < 3) {
-        const size_t i = (size_t)s * kXSlotWords + q;
+        const size_t a = (size_t)s * kXSlotWords + q;
         if (sys)
-          ld_poll1s(base + i, w[k]);
+          ld_poll1s(base + a, w[k]);
         else
-          ld_poll1(base + i, w[k]);
-        ok = ok && ((w[k] - prev[i]) & ~kDataMask) == target;
+          ld_poll1(base + a, w[k]);
+        ok = ok && ((w[k] - prev[s * 4 + q]) & ~kDataMask) == target;
       }
     }
     done = __all_sync(0xffffffffu, ok);
@@ -568,9 +568,8 @@ __device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns,
     const int s = 8 * (k0 + k) + (lane >> 2);
     unsigned long long d = 0ull;
     if (s < ns && q < 3) {
-      const size_t i = (size_t)s * kXSlotWords + q;
-      d = (w[k] - prev[i]) & kDataMask;
-      prev[i] = w[k];
+      d = (w[k] - prev[s * 4 + q]) & kDataMask;
+      prev[s * 4 + q] = w[k];
     }
     const unsigned long long d1 = __shfl_down_sync(0xffffffffu, d, 1), d2 = __shfl_down_sync(0xffffffffu, d, 2);
     tot[k] = from_limbs(d, d1, d2);
@@ -1364,7 +1363,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     if (e == m && G.cta == 0) {  // the next sweep's exchange baselines
       if (lane == 0) c.xsnap[0] = xbase + (unsigned long long)(m + 1);
       const unsigned long long *src = &S.xprev[0][0];
-      for (int i = lane; i < kXSets * (int)kXSetWords; i += 32) c.xsnap[1 + i] = src[i];
+      for (int i = lane; i < kXSets * (int)kXPrevWords; i += 32) c.xsnap[1 + i] = src[i];
       const unsigned long long *cs = &S.cprev[0][0];
       for (int i = lane; i < kCSets * (int)kCSetWords; i += 32) c.csnap[i] = cs[i];
     }
@@ -1412,7 +1411,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   for (int i = tid; i < c.m; i += kSweepThreads) G.hdr[i] = c.hdr[i];
   {  // exchange baselines: the words' values when the previous sweep ended
     unsigned long long *dst = &S.xprev[0][0];
-    for (int i = tid; i < kXSets * (int)kXSetWords; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
+    for (int i = tid; i < kXSets * (int)kXPrevWords; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
     unsigned long long *cd = &S.cprev[0][0];
     for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cd[i] = c.csnap[i];
   }

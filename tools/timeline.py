@@ -8,7 +8,7 @@ import sys, os
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2410_23244_b200 import _build
-os.environ["BART_LIB"] = _build.build_timeline()  # instrumented variant (BART_TIMELINE=1)
+os.environ["BART_LIB"] = _build.build_timeline(tuple(os.environ.get("BART_TL_DEFINES", "").split()))  # instrumented variant
 from paper_2410_23244_b200 import _native as N
 from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
 from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
@@ -42,6 +42,9 @@ print("decide: division              ", q(t[:, 9] - t[:, 8]))
 print("decide: accept known          ", q(t[:, 10] - t[:, 9]))
 print("decide: deltas + arrive       ", q(t[:, 11] - t[:, 10]))
 print("worker: decision->A start     ", q(t[:, 0][1:] - t[:, 11][:-1]))
+print("  ctrl arrive -> worker sync ret", q(t[:, 3] - t[:, 11]))
+print("  worker sync ret -> A start    ", q(t[:, 0][1:] - t[:, 3][:-1]))
+print("  worker B done -> ctrl arrive  ", q(t[:, 11] - t[:, 2]))
 print("helper prepare(e+1) done      ", q(t[:, 13] - t[:, 12]))
 print("tree period (cycles)          ", q(np.diff(t[:, 4])))
 nb = st.sweep_config()["ctas"]
