@@ -132,7 +132,7 @@ int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struc
 int bart_set_taps(bart_chain *h, int on);
 int bart_get_taps(bart_chain *h, int64_t *counts, double *sums);
 int64_t bart_iteration(bart_chain *h);
-/* Tracing: per-tree phase stamps (clock64) of the last sweep, layout (3, m+1, 8):
+/* Tracing: per-tree phase stamps (clock64) of the last sweep, (m+2) rows of 32 (buffer 4*(m+2)*8 words):
  * [0] CTA 0 and [1] last CTA: start, data-ready, pass-done, block-reduced, -,
  * gathered, gathered-synced, decided; [2] CTA 0 stamps inside the decision. */
 int bart_set_timeline(bart_chain *h, int on);

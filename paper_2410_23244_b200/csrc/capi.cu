@@ -837,7 +837,7 @@ int bart_set_timeline(bart_chain *h, int on) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
-  if (on && !h->timeline_buf) CUDA_TRY(own(h, &h->timeline_buf, (size_t)3 * (c.m + 2) * 8));
+  if (on && !h->timeline_buf) CUDA_TRY(own(h, &h->timeline_buf, (size_t)4 * (c.m + 2) * 8));
   if (on && !h->trace_buf) CUDA_TRY(own(h, &h->trace_buf, (size_t)(c.m + 2) * c.nblk * 2));
   c.timeline = on ? h->timeline_buf : nullptr;
   c.trace = on ? h->trace_buf : nullptr;
@@ -851,7 +851,7 @@ int bart_set_timeline(bart_chain *h, int on) {
 int bart_get_timeline(bart_chain *h, int64_t *out) {
   if (int rc = bart_sync(h)) return rc;
   if (!h->timeline_buf) return fail(BART_ESTATE, "timeline not enabled (bart_set_timeline)");
-  CUDA_TRY(cudaMemcpy(out, h->timeline_buf, (size_t)3 * (h->c.m + 2) * 8 * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->timeline_buf, (size_t)4 * (h->c.m + 2) * 8 * 8, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 

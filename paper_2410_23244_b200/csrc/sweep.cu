@@ -323,8 +323,20 @@ __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)
     case 2: sums_pass<W, 1, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
     case 3: sums_pass<W, 2, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
     case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+#ifndef BART_SUMS_WIDE_VARIANTS
+#define BART_SUMS_WIDE_VARIANTS 1
+#endif
+#if BART_SUMS_WIDE_VARIANTS
+    // one variant per width: a compared slot costs ~300 cycles per pass
+    // (tools/apass_bench.cu), more than the variants' instruction-cache cost
+    case 5: sums_pass<W, 4, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 6: sums_pass<W, 5, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 7: sums_pass<W, 6, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+#else
     case 5: case 6: case 7: case 8:
       sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+#endif
     default:
       sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
       for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
@@ -967,7 +979,7 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
     if (lane == 0) mbar_arrive(&S.cnt_mbar[0]);
   }
   for (int e = -1; e <= m; ++e) {
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 0] = gtimer_after((double)S.flag_t);  // after the barrier releases
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 0] = gtimer_after((double)S.flag_t);  // after the barrier releases
     // ---- A_e: critical path
     if (e >= 0 && e < m) {
       APass A;
@@ -979,6 +991,13 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       A.slots = rec_hdr(G.rec(e)).slot_node;
       A.ns = G.hdr[e].nslots;
       sums_passes<W>(r, lp, lc, A, G, S.dlt, S, tid, warp, lane);
+#if BART_TIMELINE
+      if (lane == 0 && G.cta == 0 && c.timeline) {  // every worker warp's A-pass end
+        const volatile double dep = S.wsum[warp][0];
+        (void)dep;
+        c.timeline[(size_t)(e + 1) * 32 + 16 + warp] = gtimer();
+      }
+#endif
       named_arrive(BAR_PARTIALS, kBarWC);
     } else if (e == m) {  // tree m-1's update, residual write-back, sum of squares (sampler.py:790-794)
       const bool wr = m > 0 && S.flag_wr, prune = S.flag_prune;
@@ -1005,7 +1024,7 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       named_arrive(BAR_PARTIALS, kBarWC);
       break;
     }
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 1] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 1] = gtimer();
     // ---- B_e: tree e+2's refresh + counts, hidden behind the exchange
     uint32_t lnn[W];
     const int j2 = e + 2;
@@ -1026,9 +1045,9 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       lc[k] = ln[k];
       ln[k] = lnn[k];
     }
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 2] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 2] = gtimer();
     if (e >= 0) named_sync(BAR_DECISION, kBarWC);  // decision of tree e installed (S.dlt, flags)
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 3] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 3] = gtimer();
   }
 }
 
@@ -1114,6 +1133,7 @@ __device__ __forceinline__ void stream_sums_all(const ChainDev &c, const Geom &G
     case 3: stream_sums<2, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
     case 4: stream_sums<3, true>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true); break;
     default:  // wide trees: further passes re-read the (updated) residuals
+      // (per-width variants here cost 28% at n = 1e7: the stream loop spills)
       stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true);
       for (int base = 8; base < A.ns; base += 8)
         stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, base, false);
@@ -1258,7 +1278,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 
     named_sync(BAR_PARTIALS, kBarWC);  // A_e partials complete
     // (BAR.SYNC defers blocking to the next dependent instruction: stamp after a shared load)
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 4] = gtimer_after(S.wsum[0][0]);
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 4] = gtimer_after(S.wsum[0][0]);
 #if BART_TIMELINE
     if (c.trace && lane == 0) {
       const volatile double dep = S.wsum[0][0];
@@ -1266,7 +1286,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
       c.trace[((size_t)(e + 1) * G.nblk + G.cta) * 2 + 0] = nstimer();
     }
 #endif
-    long long *ts = tl ? tl + (size_t)(e + 1) * 16 : nullptr;
+    long long *ts = tl ? tl + (size_t)(e + 1) * 32 : nullptr;
     exchange_add(c, X, S, ns, set, lane, ts);
     TL_STAMP(ts) ts[5] = gtimer();
     DecIn I;
@@ -1295,7 +1315,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
         named_arrive(BAR_DECISION, kBarWC);
       }
     }
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 12] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 12] = gtimer();
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.dec_mbar[e & 1]);  // dec[e & 1] (or sum r^2) for the helper
   }
@@ -1348,7 +1368,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     // tree e+1's count-only terms: prep[(e+1)&1] was last read by decide(e-1)
     // and decide_post(e-1), both done
     if (e + 1 < m) prepare_tree(e + 1);
-    TL_STAMP(tl) tl[(size_t)(e + 1) * 16 + 13] = gtimer();
+    TL_STAMP(tl) tl[(size_t)(e + 1) * 32 + 13] = gtimer();
     mbar_wait(&S.dec_mbar[e & 1], par2(e));  // exchange e done, decision e taken
     if (e < m && G.cta == e % G.nblk)
       decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K, hist_row);

@@ -25,10 +25,10 @@ run(st, hp, 20); st.sync()
 N.check(N.lib().bart_set_timeline(st.handle, 1))
 ms = np.zeros(3, np.float32)
 N.check(N.lib().bart_profile(st.handle, 3, N.ptr(ms)))
-tl = np.zeros((3, m + 2, 8), np.int64)
+tl = np.zeros((4, m + 2, 8), np.int64)
 N.check(N.lib().bart_get_timeline(st.handle, N.ptr(tl)))
 print(f"n={n} p={p} m={m} sweep {ms[1]/3:.3f} ms/launch, {ms[1]/3/m*1e3:.2f} us/tree, propose {ms[2]/3*1e3:.1f} us; cfg {st.sweep_config()}")
-t = tl.reshape(-1)[: (m + 2) * 16].reshape(m + 2, 16)[1:m + 1].astype(float)  # rows: trees 0..m-1
+t = tl.reshape(-1)[: (m + 2) * 32].reshape(m + 2, 32)[1:m + 1].astype(float)  # rows: trees 0..m-1
 q = lambda a: f"{np.median(a):6.0f} (p90 {np.percentile(a, 90):6.0f})"
 print("worker  A pass                ", q(t[:, 1] - t[:, 0]))
 print("worker  B pass                ", q(t[:, 2] - t[:, 1]))
@@ -45,6 +45,11 @@ print("worker: decision->A start     ", q(t[:, 0][1:] - t[:, 11][:-1]))
 print("  ctrl arrive -> worker sync ret", q(t[:, 3] - t[:, 11]))
 print("  worker sync ret -> A start    ", q(t[:, 0][1:] - t[:, 3][:-1]))
 print("  worker B done -> ctrl arrive  ", q(t[:, 11] - t[:, 2]))
+wa = t[:, 16:30]
+print("A end spread over worker warps ", q(wa.max(1) - wa.min(1)))
+print("A start -> last warp A end     ", q(wa.max(1) - t[:, 0]))
+print("last warp A end -> ctrl synced ", q(t[:, 4] - wa.max(1)))
+print("A end by warp (median rel. to first):", np.median(wa - wa.min(1, keepdims=True), axis=0).astype(int))
 print("helper prepare(e+1) done      ", q(t[:, 13] - t[:, 12]))
 print("tree period (cycles)          ", q(np.diff(t[:, 4])))
 nb = st.sweep_config()["ctas"]
