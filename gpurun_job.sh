@@ -1,7 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_parity.log 2>&1; tail -3 gpurun_out/pytest_parity.log
-timeout 900 python tools/variants.py bench s32 base s32 base -- --steps 200 --warmup 5 --e2e-steps 2 > gpurun_out/var.txt 2>&1
-timeout 900 python tools/variants.py bench s32 base -- --steps 1000 --warmup 5 --e2e-steps 2 >> gpurun_out/var.txt 2>&1
-timeout 600 python tools/variants.py bench s32 base -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 >> gpurun_out/var.txt 2>&1
-timeout 600 python tools/variants.py bench s32 base -- --n 10000000 --steps 10 --warmup 3 --e2e-steps 1 >> gpurun_out/var.txt 2>&1
-cat gpurun_out/var.txt
+timeout 900 python -m pytest tests/test_gpu_serialize.py tests/test_gpu_fit.py -x -q > gpurun_out/pytest_ser.log 2>&1; tail -25 gpurun_out/pytest_ser.log

@@ -132,6 +132,10 @@ int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struc
 int bart_set_taps(bart_chain *h, int on);
 int bart_get_taps(bart_chain *h, int64_t *counts, double *sums);
 int64_t bart_iteration(bart_chain *h);
+/* Resume support (checkpoints): set the iteration counter, which is also the
+ * device random stream's Philox counter, so a restored chain continues the
+ * stream it was saved from. */
+int bart_set_iteration(bart_chain *h, int64_t iteration);
 /* Tracing: per-tree phase stamps (clock64) of the last sweep, (m+2) rows of 32 (buffer 4*(m+2)*8 words):
  * [0] CTA 0 and [1] last CTA: start, data-ready, pass-done, block-reduced, -,
  * gathered, gathered-synced, decided; [2] CTA 0 stamps inside the decision. */
@@ -163,6 +167,9 @@ int bart_trace_counts(bart_chain *h, int64_t *n_iter, int64_t *n_keep);
 int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, double *sigma2_keep, double *train_mean,
                     double *train_var, double *train_draws, double *train_points, double *test_draws,
                     double *mean_leaves, uint16_t *axis, uint8_t *cutpoint, float *leaf_value);
+/* kept draws [k0, k1) only: train (k1-k0, n) / test (k1-k0, n_test), either NULL
+ * (streams a BFTRACE1 file from the device without one host array of every draw) */
+int bart_trace_read_draws(bart_chain *h, int64_t k0, int64_t k1, double *train, double *test);
 int bart_trace_end(bart_chain *h);
 
 /* ---- predictions (trees.sum_leaf_values / evaluate_forest, trees.py:206-223) ---- */

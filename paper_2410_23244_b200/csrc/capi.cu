@@ -593,6 +593,22 @@ int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, doubl
   return BART_OK;
 }
 
+int bart_trace_read_draws(bart_chain *h, int64_t k0, int64_t k1, double *train, double *test) {
+  int64_t ni = 0, nk = 0;
+  if (int rc = bart_trace_counts(h, &ni, &nk)) return rc;
+  if (k0 < 0 || k1 < k0 || k1 > nk) return fail(BART_EINVAL, "draw range outside the kept draws");
+  const TraceState &t = h->tr;
+  if (train && !t.store_train) return fail(BART_ESTATE, "training-row draws were not stored (store_train_draws)");
+  if (test && !t.n_test) return fail(BART_ESTATE, "no test rows in this trace");
+  if (int rc = bart_sync(h)) return rc;
+  const size_t rows = (size_t)(k1 - k0);
+  if (train && rows)
+    CUDA_TRY(cudaMemcpy(train, t.train + (size_t)k0 * h->c.n, rows * h->c.n * 8, cudaMemcpyDeviceToHost));
+  if (test && rows)
+    CUDA_TRY(cudaMemcpy(test, t.test + (size_t)k0 * t.n_test, rows * t.n_test * 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
 int bart_trace_end(bart_chain *h) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   CUDA_TRY(cudaSetDevice(h->device));
@@ -872,6 +888,18 @@ int bart_get_taps(bart_chain *h, int64_t *counts, double *sums) {
 }
 
 int64_t bart_iteration(bart_chain *h) { return h ? h->iteration : -1; }
+
+int bart_set_iteration(bart_chain *h, int64_t iteration) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  if (iteration < 0) return fail(BART_EINVAL, "iteration must be >= 0");
+  if (h->tr.on) return fail(BART_ESTATE, "cannot move the iteration counter while a trace is recording");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  const unsigned long long it = (unsigned long long)iteration;  // the device Philox counter
+  CUDA_TRY(cudaMemcpy(h->c.iter_dev, &it, sizeof(it), cudaMemcpyHostToDevice));
+  h->iteration = iteration;
+  return BART_OK;
+}
 int64_t bart_kernel_launches(bart_chain *h) { return h ? h->launches : -1; }
 
 int bart_sweep_config(bart_chain *h, int32_t *out) {

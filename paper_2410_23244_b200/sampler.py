@@ -295,6 +295,20 @@ class SamplerState:
         lo, hi = availability_intervals(self.forest, self.max_cuts)
         return (hi > lo).any(axis=2)
 
+    # -- resume
+    def restore(self, forest: Forest, leaf_index: np.ndarray, resid: np.ndarray, sigma2: float,
+                iteration: int) -> None:
+        """Install a saved chain state (serialize.load_checkpoint): the forest,
+        the (n, m) leaf-index cache, residuals, sigma^2 and the iteration (the
+        device random stream's counter)."""
+        self.forest = forest
+        self.leaf_index = leaf_index
+        self.resid = resid
+        self.sigma2 = sigma2
+        self._push()
+        N.check(N.lib().bart_set_iteration(self._h, int(iteration)))
+        self.iteration = int(iteration)
+
     # -- pushing host edits
     def rebuild_structure_caches(self) -> None:
         """Make the device state match the host mirrors (sampler.py:157-168)."""
@@ -393,8 +407,9 @@ class SamplerState:
         """Record the current state as a kept draw (asynchronous)."""
         N.check(N.lib().bart_trace_keep(self._h))
 
-    def trace_read(self) -> dict:
-        """Everything recorded since trace_begin, in the reference's layouts (scaled units)."""
+    def trace_read(self, train_draws: bool = True) -> dict:
+        """Everything recorded since trace_begin, in the reference's layouts (scaled units);
+        train_draws=False leaves the (n_keep, n) draws on the device (trace_read_draws)."""
         ni, nk = C.c_int64(), C.c_int64()
         N.check(N.lib().bart_trace_counts(self._h, C.byref(ni), C.byref(nk)))
         ni, nk, n, m, D = ni.value, nk.value, self.y.size, self._m, self._D
@@ -402,7 +417,7 @@ class SamplerState:
         out = dict(
             accepted=np.empty((ni, m), np.uint8), sigma2_iter=np.empty(ni), sigma2_keep=np.empty(nk),
             train_mean=np.empty(n), train_var=np.empty(n),
-            train_draws=np.empty((nk, n)) if o["store_train"] else None,
+            train_draws=np.empty((nk, n)) if o["store_train"] and train_draws else None,
             train_points=np.empty((nk, min(n, N.TRACE_POINTS))),
             test_draws=np.empty((nk, o["n_test"])) if o["n_test"] else None,
             mean_leaves=np.empty(nk),
@@ -414,6 +429,14 @@ class SamplerState:
         N.check(N.lib().bart_trace_read(self._h, *[N.ptr(out[k]) for k in keys]))
         out["accepted"] = out["accepted"].astype(bool)
         return out
+
+    def trace_read_draws(self, k0: int, k1: int, train: bool = True, test: bool = False):
+        """Kept draws [k0, k1) of the training-row (and test-row) predictions, scaled units."""
+        n_test = self._trace["n_test"]
+        tr = np.empty((k1 - k0, self.y.size)) if train else None
+        te = np.empty((k1 - k0, n_test)) if test else None
+        N.check(N.lib().bart_trace_read_draws(self._h, int(k0), int(k1), N.ptr(tr), N.ptr(te)))
+        return tr, te
 
     def trace_end(self) -> None:
         N.check(N.lib().bart_trace_end(self._h))

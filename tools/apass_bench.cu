@@ -73,7 +73,14 @@ __global__ void __launch_bounds__(kWorkers, 1) apass(const float *rin, const uin
           const double v = (VAR & 2) ? f2d_int(rv[b]) : (double)rv[b];
           tot = __dadd_rn(tot, v);
 #pragma unroll
-          for (int s = 0; s < C; ++s) acc[s] = __fma_rn(v, h == sn[s] ? 1.0 : 0.0, acc[s]);
+          for (int s = 0; s < C; ++s) {
+            if (VAR & 4)
+              asm("{.reg .pred p; setp.eq.u32 p, %1, %2; @p add.rn.f64 %0, %0, %3;}" : "+d"(acc[s]) : "r"(h), "r"(sn[s]), "d"(v));
+            else if (VAR & 8)
+              acc[s] = __dadd_rn(acc[s], h == sn[s] ? v : 0.0);
+            else
+              acc[s] = __fma_rn(v, h == sn[s] ? 1.0 : 0.0, acc[s]);
+          }
         }
       }
     }
@@ -140,6 +147,10 @@ int main() {
   }
   cudaMemcpy(r, hr.data(), words * 16, cudaMemcpyHostToDevice);
   cudaMemcpy(l, hl.data(), words * 4, cudaMemcpyHostToDevice);
+  run<4, 1, 5>(r, l, nwords, d, sink, "guarded, predicated DADD");
+  run<4, 3, 5>(r, l, nwords, d, sink, "guarded, predicated DADD");
+  run<4, 7, 5>(r, l, nwords, d, sink, "guarded, predicated DADD");
+  run<4, 3, 9>(r, l, nwords, d, sink, "guarded, select DADD");
   run<4, 1, 1>(r, l, nwords, d, sink, "guarded (sweep v8)");
   run<4, 1, 0>(r, l, nwords, d, sink, "unguarded");
   run<4, 1, 3>(r, l, nwords, d, sink, "guarded, int f2d");
