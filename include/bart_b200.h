@@ -74,6 +74,12 @@ typedef struct {
 int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X,
                 const int64_t *max_cuts, const float *y, double sigma2, uint64_t seed,
                 int device, bart_chain **out);
+/* Multi-chain batching: the same, with the chain's sweep
+ * limited to max_ctas CTAs (= SMs; 0: no limit), so several chains, each on
+ * its own stream, co-run on one GPU instead of taking turns. */
+int bart_device_sms(int device); /* SM count (-1 without a device) */
+int bart_create_ex(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
+                   const float *y, double sigma2, uint64_t seed, int device, int max_ctas, bart_chain **out);
 int bart_destroy(bart_chain *h);
 
 /* ---- n-sharding across GPUs (the reference has none: PAPER.md:405-409) ----

@@ -48,6 +48,8 @@ class Randoms(C.Structure):
 _P = C.c_void_p
 _SIGS = {
     "bart_create": [C.POINTER(Dims), C.POINTER(HParams), _P, _P, _P, C.c_double, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)],
+    "bart_create_ex": [C.POINTER(Dims), C.POINTER(HParams), _P, _P, _P, C.c_double, C.c_uint64, C.c_int, C.c_int,
+                       C.POINTER(C.c_void_p)],
     "bart_destroy": [_P],
     "bart_create_shard": [C.POINTER(Dims), C.c_int64, C.c_int, C.c_int, C.POINTER(HParams), _P, _P, _P, C.c_double,
                           C.c_uint64, C.c_int, C.POINTER(C.c_void_p)],
@@ -93,8 +95,9 @@ _SIGS = {
     "bart_graph_active": [_P],
 }
 _I64 = {"bart_iteration": [_P], "bart_kernel_launches": [_P]}
+_I32 = {"bart_device_sms": [C.c_int]}
 _STR = {"bart_last_error": [], "bart_version": []}
-EXPORTS = sorted(list(_SIGS) + list(_I64) + list(_STR))
+EXPORTS = sorted(list(_SIGS) + list(_I64) + list(_I32) + list(_STR))
 
 _lib = None
 
@@ -121,6 +124,10 @@ def load_library(path: str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int64
+    for name, args in _I32.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
     for name, args in _STR.items():
         fn = getattr(lib, name)
         fn.argtypes = args

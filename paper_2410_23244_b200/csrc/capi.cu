@@ -201,7 +201,7 @@ const char *bart_version(void) { return "bart_b200 0.1 sm_100a"; }
 
 static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_shards, const bart_hparams *hp,
                        const uint8_t *X, const int64_t *max_cuts, const float *y, double sigma2, uint64_t seed,
-                       int device, bart_chain **out) {
+                       int device, bart_chain **out, int max_ctas = 0) {
   if (int rc = check_dims(dims)) return rc;
   if (n_shards < 1 || n_shards > kMaxShards || shard < 0 || shard >= n_shards)
     return fail(BART_EINVAL, "shard must be in [0, n_shards), n_shards in [1, " + std::to_string(kMaxShards) + "]");
@@ -239,6 +239,7 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   int64_t want = (c.n + 1023) / 1024;
   int nblk = (int)(want < sms ? (want > 0 ? want : 1) : sms);
   if (nblk > kMaxCtas) nblk = kMaxCtas;
+  if (max_ctas > 0 && nblk > max_ctas) nblk = max_ctas;  // multi-chain batching: leave SMs to other chains
   int64_t chunk = round16((c.n + nblk - 1) / nblk);
   nblk = (int)((c.n + chunk - 1) / chunk);
   c.nblk = nblk;
@@ -376,6 +377,21 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
 int bart_create(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
                 const float *y, double sigma2, uint64_t seed, int device, bart_chain **out) {
   return create_impl(dims, dims ? dims->n : 0, 0, 1, hp, X, max_cuts, y, sigma2, seed, device, out);
+}
+
+int bart_device_sms(int device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    fail(BART_ECUDA, "no CUDA device");
+    return -1;
+  }
+  return sms;
+}
+
+int bart_create_ex(const bart_dims *dims, const bart_hparams *hp, const uint8_t *X, const int64_t *max_cuts,
+                   const float *y, double sigma2, uint64_t seed, int device, int max_ctas, bart_chain **out) {
+  if (max_ctas < 0) return fail(BART_EINVAL, "max_ctas must be >= 0");
+  return create_impl(dims, dims ? dims->n : 0, 0, 1, hp, X, max_cuts, y, sigma2, seed, device, out, max_ctas);
 }
 
 int bart_create_shard(const bart_dims *dims, int64_t n_total, int shard, int n_shards, const bart_hparams *hp,

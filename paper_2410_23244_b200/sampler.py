@@ -170,7 +170,7 @@ class SamplerState:
     """
 
     def __init__(self, X, max_cuts, y, hp: Hyperparams, rng, sigma2: float, device: int = 0,
-                 shard: tuple[int, int, int] | None = None):
+                 shard: tuple[int, int, int] | None = None, max_ctas: int | None = None):
         self.X = X
         self.max_cuts = max_cuts
         self.y = y
@@ -187,8 +187,9 @@ class SamplerState:
         d = N.dims(X.shape[0], X.shape[1], self._m, self._D)
         self.shard = shard  # (n_total, shard index, n_shards) for an n-sharded chain (paper_2410_23244_b200.shard)
         if shard is None:
-            N.check(N.lib().bart_create(d, N.hparams(hp, depth_probabilities(hp)), N.ptr(X), N.ptr(max_cuts),
-                                        N.ptr(y), float(sigma2), seed, self.device, C.byref(self._h)))
+            N.check(N.lib().bart_create_ex(d, N.hparams(hp, depth_probabilities(hp)), N.ptr(X), N.ptr(max_cuts),
+                                           N.ptr(y), float(sigma2), seed, self.device, int(max_ctas or 0),
+                                           C.byref(self._h)))
         else:
             n_total, k, n_shards = shard
             N.check(N.lib().bart_create_shard(d, int(n_total), int(k), int(n_shards),
@@ -459,8 +460,11 @@ class SamplerState:
 
 
 def init_state(X: np.ndarray, max_cuts: np.ndarray, y: np.ndarray, hp: Hyperparams, rng,
-               sigma2: float | None = None, device: int = 0) -> SamplerState:
-    """Fresh chain on the device: root-only zero forest, resid = y (sampler.py:201-241)."""
+               sigma2: float | None = None, device: int = 0, max_ctas: int | None = None) -> SamplerState:
+    """Fresh chain on the device: root-only zero forest, resid = y (sampler.py:201-241).
+
+    max_ctas limits the chain's sweep to that many SMs, so several chains on
+    their own streams run side by side (multi-chain batching)."""
     X = np.ascontiguousarray(X, np.uint8)
     y32 = np.ascontiguousarray(y, np.float32)
     max_cuts = np.ascontiguousarray(max_cuts, np.int64)
@@ -476,7 +480,7 @@ def init_state(X: np.ndarray, max_cuts: np.ndarray, y: np.ndarray, hp: Hyperpara
         raise ValueError(f"n_trees must be >= 1, got {hp.n_trees}")
     if sigma2 is None:
         sigma2 = float(np.var(y32, ddof=1)) if n >= 2 else 1.0
-    return SamplerState(X, max_cuts, y32, hp, rng, float(sigma2), device)
+    return SamplerState(X, max_cuts, y32, hp, rng, float(sigma2), device, max_ctas=max_ctas)
 
 
 def _randoms_struct(rnd: StepRandoms):

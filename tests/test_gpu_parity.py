@@ -143,8 +143,10 @@ def sweep_mode(request, monkeypatch):
     return request.param
 
 
-def test_chain_matches_oracle_friedman_multi_cta(sweep_mode):
-    """n=20000 spans many CTAs: 12 steps vs the oracle with the same injected randoms."""
+@pytest.mark.parametrize("max_ctas", [None, 5])
+def test_chain_matches_oracle_friedman_multi_cta(sweep_mode, max_ctas):
+    """n=20000 spans many CTAs: 12 steps vs the oracle with the same injected randoms
+    (max_ctas: the chain squeezed onto 5 SMs, as multi-chain batching does)."""
     from paper_2410_23244_b200.dgp import friedman1
     from paper_2410_23244_b200.grid import build_grid_uniform, quantize
     from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
@@ -154,8 +156,8 @@ def test_chain_matches_oracle_friedman_multi_cta(sweep_mode):
     Xq = quantize(X, g).data
     hp, ys = derive_hyperparams(y, FitConfig(n_trees=40))
     y32 = ys.forward(y).astype(np.float32)
-    st = init_state(Xq, g.counts, y32, hp, None)
-    assert st.sweep_config()["ctas"] > 1
+    st = init_state(Xq, g.counts, y32, hp, None, max_ctas=max_ctas)
+    assert st.sweep_config()["ctas"] == (5 if max_ctas else 20)
     assert st.sweep_config()["stream"] == (sweep_mode == "stream")
     st.enable_taps(True)
     ora = OracleChain(Xq, g.counts, y32, hp)
