@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "multi_cta" > gpurun_out/pytest_mc.log 2>&1; tail -3 gpurun_out/pytest_mc.log
-for cfg in "100000 4" "100000 2" "1000000 2" "1000000 4" "10000 8"; do timeout 300 python tools/multichain_bench.py $cfg 200 2>&1 | tail -5; done > gpurun_out/multichain.txt
-cat gpurun_out/multichain.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_parity.log 2>&1; tail -3 gpurun_out/pytest_parity.log
+timeout 900 python tools/variants.py bench pre_ctrl early plane base pre_ctrl early plane base -- --steps 200 --warmup 5 --e2e-steps 2 > gpurun_out/var.txt 2>&1
+timeout 600 python tools/variants.py bench pre_ctrl base -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 >> gpurun_out/var.txt 2>&1
+cat gpurun_out/var.txt
