@@ -533,6 +533,7 @@ __device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx &X, c
           red_add(X.xacc + set_off + (size_t)s * kXSlotWords + q, v, false);
         else
           for (int g = 0; g < X.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, v, sys);
+        TL_STAMP(ts && s0 == 0) ts[30] = gtimer();
       }
     }
   }

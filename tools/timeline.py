@@ -35,6 +35,8 @@ print("worker  B pass                ", q(t[:, 2] - t[:, 1]))
 print("worker0 published -> fold done", q(t[:, 14] - t[:, 1]))
 print("fold -> limbs                 ", q(t[:, 15] - t[:, 14]))
 print("limbs -> adds issued          ", q(t[:, 5] - t[:, 15]))
+print("  limbs -> red issued          ", q(t[:, 30] - t[:, 15]))
+print("  red issued -> add loop exit  ", q(t[:, 5] - t[:, 30]))
 print("adds -> prep loaded           ", q(t[:, 6] - t[:, 5]))
 print("prep -> poll complete         ", q(t[:, 7] - t[:, 6]))
 print("poll -> totals (gather/limbs) ", q(t[:, 8] - t[:, 7]))
