@@ -218,6 +218,27 @@ def barrier(world: int):
         dist.barrier()
 
 
+def profile_forest_kernels(st, N, args, reps: int = 10) -> dict:
+    """The reference's traverse_forest / sum_leaf_values / evaluate_forest
+    kernels (trees.py:174-223) on the chain's current forest, per launch, with
+    their algorithmic bytes: traverse reads each split column a tree uses once
+    (n B per distinct axis) and writes the (m, n) u8 cache; the cached sum reads
+    the cache and writes n f64; the fused one reads the columns and writes n f64."""
+    ms = np.zeros(3, np.float32)
+    N.check(N.lib().bart_profile_forest(st.handle, reps, N.ptr(ms)))
+    f = st.forest
+    n, m = args.n, args.m
+    cols = sum(len(set(int(a) for a, c in zip(f.axis[j], f.cutpoint[j]) if c > 0)) for j in range(m))
+    peak, _ = measured_peak()
+    out = {}
+    for k, (name, nbytes) in enumerate([("traverse", n * cols + n * m), ("predict_cached", n * m + 8 * n),
+                                        ("evaluate", n * cols + 8 * n)]):
+        gbs = nbytes / (float(ms[k]) / 1e3) / 1e9
+        out[name] = {"ms": float(ms[k]), "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak}
+    out["split_columns_in_forest"] = cols
+    return out
+
+
 def run_ours(args):
     world, rank, local = dist_setup(args)
     from paper_2410_23244_b200 import _build
@@ -284,6 +305,7 @@ def run_ours(args):
     e2e_s = allreduce_max(time.perf_counter() - t0, world)
     e2e = (1 if sharded else world) * args.e2e_steps / e2e_s
     graph = bool(N.lib().bart_graph_active(st.handle))
+    forest_kernels = profile_forest_kernels(st, N, args) if rank == 0 and not sharded else None
     st.close()
 
     cpu = None
@@ -321,6 +343,7 @@ def run_ours(args):
             "cuda_graph": graph,
             "sweep_grid": cfg,
             "clocks": clk.summary(),
+            "forest_kernels": forest_kernels,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

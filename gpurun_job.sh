@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-timeout 900 python tools/variants.py bench v9 base v9 base -- --steps 200 --warmup 5 --e2e-steps 2
-timeout 900 python tools/variants.py bench v9 base -- --steps 1000 --warmup 5 --e2e-steps 2
-timeout 600 python tools/variants.py bench v9 base -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python bench.py --no-cpu > gpurun_out/bench_fk.json 2>gpurun_out/bench_fk.err; python -c "
+import json; d=json.load(open('gpurun_out/bench_fk.json')); print(d['value']); print(json.dumps(d['forest_kernels'], indent=1))"; tail -3 gpurun_out/bench_fk.err

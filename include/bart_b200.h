@@ -202,6 +202,12 @@ int bart_sum_leaf_values(const bart_dims *dims, const float *leaf_value, const u
  * ms[0] = total elapsed, ms[1] = summed sweep-kernel time, ms[2] = summed
  * propose-kernel time (per-launch events, not graph-replayed). */
 int bart_profile(bart_chain *h, int64_t n_iter, float *ms);
+/* Per-launch time (ms, CUDA events on the chain's stream, `reps` back-to-back
+ * launches after a warm-up) of the forest kernels on the chain's own state:
+ * ms[0] traverse (trees.traverse_forest into a scratch cache), ms[1] cached
+ * sum of trees (trees.sum_leaf_values), ms[2] fused traverse + sum
+ * (trees.evaluate_forest). */
+int bart_profile_forest(bart_chain *h, int reps, float *ms);
 /* n_iter graph-replayed device-RNG iterations bracketed by CUDA events on the
  * chain's stream (synchronised on both sides); *ms = elapsed. */
 int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms);

@@ -1095,6 +1095,41 @@ int bart_graph_active(bart_chain *h) { return h && h->graph ? 1 : 0; }
 
 
 
+int bart_profile_forest(bart_chain *h, int reps, float *ms) {
+  if (!h || !ms || reps < 1) return fail(BART_EINVAL, "bad arguments");
+  if (int rc = bart_sync(h)) return rc;
+  const ChainDev &c = h->c;
+  DevBuf L2, pred;
+  CUDA_TRY(L2.alloc((size_t)c.m * c.n_pad));
+  CUDA_TRY(pred.alloc((size_t)c.n_pad * 8));
+  cudaEvent_t e[4];
+  for (auto &x : e) CUDA_TRY(cudaEventCreate(&x));
+  auto traverse = [&] { launch_traverse(c.Xt, c.n, c.n_pad, c.D, c.half, c.m, c.axis, c.cut, L2.as<uint8_t>(), h->stream); };
+  auto predict = [&] { launch_predict_cached(c.L, c.n, c.n_pad, c.m, c.size, c.leaf, pred.as<double>(), h->stream); };
+  auto evaluate = [&] {
+    launch_evaluate(c.Xt, c.n, c.n_pad, c.D, c.half, c.m, c.axis, c.cut, c.leaf, pred.as<double>(), h->stream);
+  };
+  traverse();  // warm-up
+  predict();
+  evaluate();
+  CUDA_TRY(cudaEventRecord(e[0], h->stream));
+  for (int i = 0; i < reps; ++i) traverse();
+  CUDA_TRY(cudaEventRecord(e[1], h->stream));
+  for (int i = 0; i < reps; ++i) predict();
+  CUDA_TRY(cudaEventRecord(e[2], h->stream));
+  for (int i = 0; i < reps; ++i) evaluate();
+  CUDA_TRY(cudaEventRecord(e[3], h->stream));
+  CUDA_TRY(cudaEventSynchronize(e[3]));
+  CUDA_TRY(cudaGetLastError());
+  for (int k = 0; k < 3; ++k) {
+    CUDA_TRY(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
+    ms[k] /= (float)reps;
+  }
+  for (auto &x : e) cudaEventDestroy(x);
+  h->launches += 3 * (int64_t)(reps + 1);
+  return BART_OK;
+}
+
 int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
   if (!h || !ms) return fail(BART_EINVAL, "NULL argument");
   CUDA_TRY(cudaSetDevice(h->device));
