@@ -1,3 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python bench.py --no-cpu > gpurun_out/bench_fk.json 2>gpurun_out/bench_fk.err; python -c "
-import json; d=json.load(open('gpurun_out/bench_fk.json')); print(d['value']); print(json.dumps(d['forest_kernels'], indent=1))"; tail -3 gpurun_out/bench_fk.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_t.csv python bench.py --steps 5 --warmup 3 --e2e-steps 2 --no-cpu > /dev/null 2>&1
+grep -i "transpose\|memset" gpurun_out/launches_t.csv | cut -c1-200 | head -5

@@ -26,30 +26,77 @@
 
 namespace bart {
 
-// dst[c * dst_ld + r] = src[r * src_ld + c] for r < rows, c < cols; one
-// 32x32 tile per CTA over a 1-D grid (either dimension may exceed 65535 tiles)
-__global__ void transpose_u8_kernel(const uint8_t *__restrict__ src, int64_t rows, int64_t cols, int64_t src_ld,
-                                    uint8_t *__restrict__ dst, int64_t dst_ld, int64_t col_tiles) {
-  __shared__ uint8_t tile[32][33];
+// dst[c * dst_ld + r] = src[r * src_ld + c] for r < rows, c < cols.
+// 64 x 64-byte tiles over a 1-D grid (either dimension may exceed 65535
+// tiles); 256 threads.  Loads: 4-byte words when rows are 4-byte aligned
+// (W4), else bytes; stores: 16-byte vectors when destination rows are 16-byte
+// aligned (V16), else bytes.  Out-of-range source bytes read as 0, so the
+// destination's padding (dst_ld > rows) is written with zeros.
+template <bool W4, bool V16>
+__global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t *__restrict__ src, int64_t rows, int64_t cols,
+                                                           int64_t src_ld, uint8_t *__restrict__ dst, int64_t dst_ld,
+                                                           int64_t col_tiles) {
+  __shared__ uint8_t tile[64][68];
   const int64_t tr = (int64_t)blockIdx.x / col_tiles, tc = (int64_t)blockIdx.x % col_tiles;
-  const int64_t r0 = tr * 32, c0 = tc * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
-  for (int k = ty; k < 32; k += 8) {
-    const int64_t r = r0 + k, cc = c0 + tx;
-    if (r < rows && cc < cols) tile[k][tx] = src[r * src_ld + cc];
+  const int64_t r0 = tr * 64, c0 = tc * 64;
+  const int t = threadIdx.x;
+  {  // load: thread t -> source row t / 4, 16 columns from (t % 4) * 16
+    const int rr = t >> 2, cc = (t & 3) * 16;
+    const int64_t r = r0 + rr;
+    uint8_t b[16];
+    if (W4 && r < rows && c0 + cc + 16 <= cols) {
+      const uint32_t *p = reinterpret_cast<const uint32_t *>(src + r * src_ld + c0 + cc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t w = __ldg(p + k);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[4 * k + q] = (uint8_t)(w >> (8 * q));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int64_t c = c0 + cc + k;
+        b[k] = (r < rows && c < cols) ? __ldg(src + r * src_ld + c) : (uint8_t)0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[rr][cc + k] = b[k];
   }
   __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int64_t cc = c0 + k, r = r0 + tx;
-    if (r < rows && cc < cols) dst[cc * dst_ld + r] = tile[tx][k];
+  {  // store: thread t -> destination row (source column) t / 4, 16 source rows from (t % 4) * 16
+    const int cc = t >> 2, rr = (t & 3) * 16;
+    const int64_t c = c0 + cc, r = r0 + rr;
+    if (c >= cols) return;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (uint32_t)tile[rr + 4 * k][cc] | ((uint32_t)tile[rr + 4 * k + 1][cc] << 8) |
+             ((uint32_t)tile[rr + 4 * k + 2][cc] << 16) | ((uint32_t)tile[rr + 4 * k + 3][cc] << 24);
+    if (V16) {
+      if (r < dst_ld) *reinterpret_cast<uint4 *>(dst + c * dst_ld + r) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (r + k < dst_ld && r + k < rows) dst[c * dst_ld + r + k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+    }
   }
 }
 
 void launch_transpose_u8(const uint8_t *src, int64_t rows, int64_t cols, int64_t src_ld, uint8_t *dst,
                          int64_t dst_ld, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return;
-  const int64_t rt = (rows + 31) / 32, ct = (cols + 31) / 32;
-  transpose_u8_kernel<<<(unsigned)(rt * ct), 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
+  const int64_t rt = (rows + 63) / 64, ct = (cols + 63) / 64;
+  const bool w4 = src_ld % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 4 == 0;
+  const bool v16 = dst_ld % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0;
+  const unsigned g = (unsigned)(rt * ct);
+  if (w4 && v16)
+    transpose_u8_kernel<true, true><<<g, 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
+  else if (w4)
+    transpose_u8_kernel<true, false><<<g, 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
+  else if (v16)
+    transpose_u8_kernel<false, true><<<g, 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
+  else
+    transpose_u8_kernel<false, false><<<g, 256, 0, s>>>(src, rows, cols, src_ld, dst, dst_ld, ct);
 }
 
 // every point at the root (1), padding points 0: two strided memsets run at
