@@ -131,6 +131,9 @@ int bart_get_leaf_index(bart_chain *h, uint8_t *out_nm); /* (n, m) */
 int bart_get_resid(bart_chain *h, float *out);
 int bart_get_sigma2(bart_chain *h, double *out);
 int bart_get_accepted(bart_chain *h, uint8_t *out); /* last_accepted (m,) */
+/* last_accepted (m,) and sigma2 after the last step in one synchronisation
+ * (either pointer may be NULL): the per-step read of the end-to-end loop */
+int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2);
 int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struct_log /* (m,) */);
 /* Phase taps for parity (enable with bart_set_taps before the step):
  * counts (m, 2^D) after the grow refresh (sampler.py:894-897) and the

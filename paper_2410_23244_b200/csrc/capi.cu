@@ -101,6 +101,9 @@ struct bart_chain {
   std::vector<void *> ipc_opened;  // peer shards' exchange buffers (cudaIpcOpenMemHandle)
   bool shard_pending = false;      // created as a shard, not yet connected
   TraceState tr;
+  double *rand_stage = nullptr;     // pinned: one injected StepRandoms block
+  uint8_t *result_stage = nullptr;  // pinned: last_accepted (m) + sigma2
+  cudaEvent_t rand_copied = nullptr;
 };
 
 namespace {
@@ -113,6 +116,10 @@ void free_chain(bart_chain *h) {
   for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : h->owned)
     if (p) cudaFree(p);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->rand_stage) cudaFreeHost(h->rand_stage);
+  if (h->result_stage) cudaFreeHost(h->result_stage);
+  if (h->rand_copied) cudaEventDestroy(h->rand_copied);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -286,10 +293,18 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   c.rstride = rec_stride(c.size);
   OWN(recs, (size_t)c.m * c.rstride);
   OWN(hdr, (size_t)c.m);
-  OWN(rm, (size_t)c.m * 5);
-  OWN(ra, (size_t)c.m);
-  OWN(rz, (size_t)c.m * c.size);
-  OWN(rc2, 1);
+  // one StepRandoms block (move_u | accept_u | leaf_z | chi2), so an injected
+  // block is one host->device copy from the pinned staging buffer
+  const size_t rwords = (size_t)c.m * 5 + (size_t)c.m + (size_t)c.m * c.size + 1;
+  OWN(rm, rwords);
+  if (e == cudaSuccess) {
+    ra = rm + (size_t)c.m * 5;
+    rz = ra + c.m;
+    rc2 = rz + (size_t)c.m * c.size;
+    e = cudaMallocHost(&h->rand_stage, rwords * 8);
+    if (e == cudaSuccess) e = cudaMallocHost(&h->result_stage, (size_t)c.m + 16);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->rand_copied, cudaEventDisableTiming);
+  }
   OWN(s2, 1);
   OWN(s2d, 1);
   OWN(acc, (size_t)c.m);
@@ -743,11 +758,17 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
   if (rnd) {
     if (!rnd->move_u || !rnd->accept_u || !rnd->leaf_z) return fail(BART_EINVAL, "incomplete randoms");
-    CUDA_TRY(cudaMemcpyAsync(c.rand_move, rnd->move_u, (size_t)c.m * 5 * 8, cudaMemcpyHostToDevice, h->stream));
-    CUDA_TRY(cudaMemcpyAsync(c.rand_acc, rnd->accept_u, (size_t)c.m * 8, cudaMemcpyHostToDevice, h->stream));
-    CUDA_TRY(cudaMemcpyAsync(c.rand_z, rnd->leaf_z, (size_t)c.m * c.size * 8, cudaMemcpyHostToDevice, h->stream));
-    CUDA_TRY(cudaMemcpyAsync(c.rand_chi2, &rnd->chi2, 8, cudaMemcpyHostToDevice, h->stream));
-    // (pageable sources: the copies are staged before cudaMemcpyAsync returns)
+    // pack into the pinned staging block (once the previous block's copy has
+    // left it) and send it with one asynchronous copy
+    CUDA_TRY(cudaEventSynchronize(h->rand_copied));
+    double *st = h->rand_stage;
+    const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
+    std::memcpy(st, rnd->move_u, nm * 8);
+    std::memcpy(st + nm, rnd->accept_u, na * 8);
+    std::memcpy(st + nm + na, rnd->leaf_z, nz * 8);
+    st[nm + na + nz] = rnd->chi2;
+    CUDA_TRY(cudaMemcpyAsync(c.rand_move, st, (nm + na + nz + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaEventRecord(h->rand_copied, h->stream));
     if (int rc = launch_iteration(h, 0)) return rc;
   } else {
     if (int rc = launch_iteration(h, 1)) return rc;
@@ -823,6 +844,20 @@ int bart_get_resid(bart_chain *h, float *out) {
 int bart_get_sigma2(bart_chain *h, double *out) {
   if (int rc = bart_sync(h)) return rc;
   CUDA_TRY(cudaMemcpy(out, h->c.sigma2, 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const size_t m = (size_t)h->c.m;
+  uint8_t *st = h->result_stage;
+  if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->c.accepted, m, cudaMemcpyDeviceToHost, h->stream));
+  if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + ((m + 7) & ~(size_t)7), h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaGetLastError());
+  if (accepted) std::memcpy(accepted, st, m);
+  if (sigma2) std::memcpy(sigma2, st + ((m + 7) & ~(size_t)7), 8);
   return BART_OK;
 }
 

@@ -235,16 +235,17 @@ class SamplerState:
         elif key == "resid":
             val = np.empty(n, np.float32)
             N.check(L.bart_get_resid(h, N.ptr(val)))
-        elif key == "sigma2":
-            v = np.empty(1, np.float64)
-            N.check(L.bart_get_sigma2(h, N.ptr(v)))
-            val = float(v[0])
-        elif key == "last_accepted":
-            if self.iteration == 0:
+        elif key in ("sigma2", "last_accepted"):
+            if key == "last_accepted" and self.iteration == 0:
                 return None
-            a = np.empty(m, np.uint8)
-            N.check(L.bart_get_accepted(h, N.ptr(a)))
-            val = a.astype(bool)
+            # both in one synchronisation: a step's result is read as a pair
+            v = np.empty(1, np.float64)
+            a = np.empty(m, np.uint8) if self.iteration > 0 else None
+            N.check(L.bart_get_step_result(h, N.ptr(a), N.ptr(v)))
+            self._cache["sigma2"] = float(v[0])
+            if a is not None:
+                self._cache["last_accepted"] = a.astype(bool)
+            val = self._cache[key]
         elif key == "last_proposals":
             if self.iteration == 0:
                 return None
