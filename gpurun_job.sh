@@ -1,2 +1,3 @@
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29562 tools/ipc_shard_check.py 20000 10 5 2>&1 | grep "ipc shard check"
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 3 --master-addr 127.0.0.1 --master-port 29563 tools/ipc_shard_check.py 7001 8 4 2>&1 | grep "ipc shard check"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'])"
+timeout 300 python tools/e2e_breakdown.py 1000000 100 2>&1 | tail -1

@@ -134,6 +134,11 @@ int bart_get_accepted(bart_chain *h, uint8_t *out); /* last_accepted (m,) */
 /* last_accepted (m,) and sigma2 after the last step in one synchronisation
  * (either pointer may be NULL): the per-step read of the end-to-end loop */
 int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2);
+/* The result (accept flags, sigma2) of bart_step number `iteration` (0-based),
+ * for either of the last two steps: every bart_step enqueues a copy of its
+ * result into pinned memory behind the step, so a caller can launch step k+1
+ * (and draw its randoms on the host meanwhile) before reading step k. */
+int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, double *sigma2);
 int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struct_log /* (m,) */);
 /* Phase taps for parity (enable with bart_set_taps before the step):
  * counts (m, 2^D) after the grow refresh (sampler.py:894-897) and the

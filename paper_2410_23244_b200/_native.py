@@ -64,6 +64,7 @@ _SIGS = {
     "bart_set_iteration": [_P, C.c_int64],
     "bart_profile_forest": [_P, C.c_int, _P],
     "bart_get_step_result": [_P, _P, _P],
+    "bart_read_step_result": [_P, C.c_int64, _P, _P],
     "bart_trace_end": [_P],
     "bart_grid_minmax": [_P, C.c_int64, C.c_int32, _P, _P, C.c_int],
     "bart_quantize": [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_int],

@@ -101,25 +101,60 @@ struct bart_chain {
   std::vector<void *> ipc_opened;  // peer shards' exchange buffers (cudaIpcOpenMemHandle)
   bool shard_pending = false;      // created as a shard, not yet connected
   TraceState tr;
-  double *rand_stage = nullptr;     // pinned: one injected StepRandoms block
   uint8_t *result_stage = nullptr;  // pinned: last_accepted (m) + sigma2
-  cudaEvent_t rand_copied = nullptr;
+  // bart_step pipeline, two slots (slot = iteration % 2): the injected random
+  // block goes host (pinned stage) -> device block on h2d, overlapping the
+  // previous step's kernel; the step's accept flags and sigma2 draw go to
+  // per-slot device buffers and come back on d2h into pinned step_out, so the
+  // host reads step k after launching step k+1.
+  double *rstage[2] = {nullptr, nullptr};
+  double *rblock[2] = {nullptr, nullptr};
+  uint8_t *acc_slot[2] = {nullptr, nullptr};
+  double *sdraw_slot[2] = {nullptr, nullptr};
+  uint8_t *res_acc = nullptr;  // where the latest step's accept flags are
+  double *res_sdraw = nullptr;
+  uint8_t *step_out = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t copy_done[2] = {nullptr, nullptr}, kernel_done[2] = {nullptr, nullptr},
+              step_out_ready[2] = {nullptr, nullptr};
+  bool update_sigma = true;
+  cudaGraphExec_t graph_step[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][injected randoms]
 };
 
 namespace {
 
+void drop_graphs(bart_chain *h) {
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  h->graph = nullptr;
+  for (auto &row : h->graph_step)
+    for (auto &g : row) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
 void free_chain(bart_chain *h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  if (h->graph) cudaGraphExecDestroy(h->graph);
+  drop_graphs(h);
   for (void *p : h->tr.bufs) cudaFree(p);
   for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void *p : h->owned)
     if (p) cudaFree(p);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  if (h->rand_stage) cudaFreeHost(h->rand_stage);
+  if (h->h2d) cudaStreamSynchronize(h->h2d);
+  if (h->d2h) cudaStreamSynchronize(h->d2h);
+  for (auto *p : h->rstage)
+    if (p) cudaFreeHost(p);
   if (h->result_stage) cudaFreeHost(h->result_stage);
-  if (h->rand_copied) cudaEventDestroy(h->rand_copied);
+  if (h->step_out) cudaFreeHost(h->step_out);
+  for (int k = 0; k < 2; ++k) {
+    if (h->copy_done[k]) cudaEventDestroy(h->copy_done[k]);
+    if (h->kernel_done[k]) cudaEventDestroy(h->kernel_done[k]);
+    if (h->step_out_ready[k]) cudaEventDestroy(h->step_out_ready[k]);
+  }
+  if (h->h2d) cudaStreamDestroy(h->h2d);
+  if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -185,10 +220,7 @@ void trace_free(bart_chain *h) {
   h->c.acc_hist = nullptr;
   h->c.sig_hist = nullptr;
   h->c.hist_cap = 0;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
 }
 template <typename T>
 cudaError_t trace_alloc(bart_chain *h, T **p, size_t count) {
@@ -296,14 +328,30 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   // one StepRandoms block (move_u | accept_u | leaf_z | chi2), so an injected
   // block is one host->device copy from the pinned staging buffer
   const size_t rwords = (size_t)c.m * 5 + (size_t)c.m + (size_t)c.m * c.size + 1;
+  double *rb1 = nullptr, *sd1 = nullptr;
+  uint8_t *acc1 = nullptr;
   OWN(rm, rwords);
+  OWN(rb1, rwords);
+  OWN(sd1, 1);
+  OWN(acc1, (size_t)c.m);
   if (e == cudaSuccess) {
     ra = rm + (size_t)c.m * 5;
     rz = ra + c.m;
     rc2 = rz + (size_t)c.m * c.size;
-    e = cudaMallocHost(&h->rand_stage, rwords * 8);
+    h->rblock[0] = rm;
+    h->rblock[1] = rb1;
+    h->sdraw_slot[1] = sd1;
+    h->acc_slot[1] = acc1;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaMallocHost(&h->rstage[k], rwords * 8);
     if (e == cudaSuccess) e = cudaMallocHost(&h->result_stage, (size_t)c.m + 16);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->rand_copied, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * (((size_t)c.m + 7) / 8 * 8 + 8));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&h->copy_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
+    }
   }
   OWN(s2, 1);
   OWN(s2d, 1);
@@ -335,6 +383,11 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   c.sigma2 = s2;
   c.sigma2_draw = s2d;
   c.accepted = acc;
+  h->acc_slot[0] = acc;
+  h->sdraw_slot[0] = s2d;
+  h->res_acc = acc;
+  h->res_sdraw = s2d;
+  h->update_sigma = hp->update_sigma != 0;
   c.xacc = xacc;
   c.xpeer[0] = xacc;
   c.n_shards = 1;
@@ -471,10 +524,7 @@ int bart_shard_connect(bart_chain *h, const void *all) {
   c.nblk_total = total;
   c.shard_sys = 1;
   h->shard_pending = false;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 
@@ -497,10 +547,7 @@ int bart_set_copy_groups(bart_chain *h, int groups) {
   c.n_shards = groups;
   c.copy_groups = groups;
   c.copy_base = 0;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 
@@ -550,10 +597,7 @@ int bart_trace_begin(bart_chain *h, const bart_trace_opts *o, const uint8_t *X_t
   c.hist_base = h->iteration;
   c.hist_cap = t.iter_cap;
   t.on = true;
-  if (h->graph) {  // the captured launch carries the trace pointers
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 
@@ -700,10 +744,8 @@ int bart_destroy(bart_chain *h) {
 int bart_set_hparams(bart_chain *h, const bart_hparams *hp) {
   if (!h || !hp) return fail(BART_EINVAL, "NULL argument");
   h->c.hp = to_hp(hp);
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  h->update_sigma = hp->update_sigma != 0;
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 
@@ -756,22 +798,80 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
   if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
+  const int slot = (int)(h->iteration & 1);
+  ChainDev args = step_args(h, rnd ? 0 : 1);
+  double *blk = h->rblock[slot];
+  const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
+  args.rand_move = blk;
+  args.rand_acc = blk + nm;
+  args.rand_z = blk + nm + na;
+  args.rand_chi2 = blk + nm + na + nz;
+  args.accepted = h->acc_slot[slot];
+  args.sigma2_draw = h->sdraw_slot[slot];
   if (rnd) {
     if (!rnd->move_u || !rnd->accept_u || !rnd->leaf_z) return fail(BART_EINVAL, "incomplete randoms");
-    // pack into the pinned staging block (once the previous block's copy has
-    // left it) and send it with one asynchronous copy
-    CUDA_TRY(cudaEventSynchronize(h->rand_copied));
-    double *st = h->rand_stage;
-    const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
+    // the slot's pinned stage is free once its last copy ran; its device block
+    // once the step two back (which read it) is done and its result is read out
+    CUDA_TRY(cudaEventSynchronize(h->copy_done[slot]));
+    double *st = h->rstage[slot];
     std::memcpy(st, rnd->move_u, nm * 8);
     std::memcpy(st + nm, rnd->accept_u, na * 8);
     std::memcpy(st + nm + na, rnd->leaf_z, nz * 8);
     st[nm + na + nz] = rnd->chi2;
-    CUDA_TRY(cudaMemcpyAsync(c.rand_move, st, (nm + na + nz + 1) * 8, cudaMemcpyHostToDevice, h->stream));
-    CUDA_TRY(cudaEventRecord(h->rand_copied, h->stream));
-    if (int rc = launch_iteration(h, 0)) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(h->h2d, h->step_out_ready[slot], 0));
+    CUDA_TRY(cudaMemcpyAsync(blk, st, (nm + na + nz + 1) * 8, cudaMemcpyHostToDevice, h->h2d));
+    CUDA_TRY(cudaEventRecord(h->copy_done[slot], h->h2d));
+    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->copy_done[slot], 0));
   } else {
-    if (int rc = launch_iteration(h, 1)) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[slot], 0));
+  }
+  // one captured launch per (slot, randoms kind): graph replay skips the
+  // cooperative launch's per-call validation
+  cudaGraphExec_t &gx = h->graph_step[slot][rnd ? 1 : 0];
+  if (!gx && !h->graph_failed) {
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const cudaError_t e1 = (cudaError_t)sweep_launch(args, h->smem, h->stream);
+      const cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+      if (e1 != cudaSuccess || e2 != cudaSuccess || !g || cudaGraphInstantiate(&gx, g, 0) != cudaSuccess) gx = nullptr;
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();
+  }
+  if (gx)
+    CUDA_TRY(cudaGraphLaunch(gx, h->stream));
+  else
+    CUDA_TRY((cudaError_t)sweep_launch(args, h->smem, h->stream));
+  h->launches += 1;
+  h->iteration += 1;
+  CUDA_TRY(cudaEventRecord(h->kernel_done[slot], h->stream));
+  h->res_acc = h->acc_slot[slot];
+  h->res_sdraw = h->sdraw_slot[slot];
+  // this step's result -> pinned step_out[slot] on d2h, behind the step
+  const size_t stride = ((size_t)c.m + 7) / 8 * 8 + 8;
+  uint8_t *dst = h->step_out + (size_t)slot * stride;
+  CUDA_TRY(cudaStreamWaitEvent(h->d2h, h->kernel_done[slot], 0));
+  CUDA_TRY(cudaMemcpyAsync(dst, h->acc_slot[slot], (size_t)c.m, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(cudaMemcpyAsync(dst + stride - 8, h->sdraw_slot[slot], 8, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(cudaEventRecord(h->step_out_ready[slot], h->d2h));
+  return BART_OK;
+}
+
+int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, double *sigma2) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  if (iteration < 0 || iteration < h->iteration - 2 || iteration >= h->iteration)
+    return fail(BART_EINVAL, "only the last two bart_step results are kept");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaEventSynchronize(h->step_out_ready[iteration & 1]));
+  const size_t stride = ((size_t)h->c.m + 7) / 8 * 8 + 8;
+  const uint8_t *src = h->step_out + (size_t)(iteration & 1) * stride;
+  if (accepted) std::memcpy(accepted, src, (size_t)h->c.m);
+  if (sigma2) {
+    if (h->update_sigma) {
+      std::memcpy(sigma2, src + stride - 8, 8);  // the step's draw became sigma2 (sampler.py:906-908)
+    } else {  // sigma2 is not sampled: the (unchanged) state value
+      CUDA_TRY(cudaMemcpy(sigma2, h->c.sigma2, 8, cudaMemcpyDeviceToHost));
+    }
   }
   return BART_OK;
 }
@@ -793,6 +893,9 @@ int bart_run(bart_chain *h, int64_t n_iter) {
   CUDA_TRY(cudaSetDevice(h->device));
   if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   ensure_graph(h);
+  for (int k = 0; k < 2; ++k) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
+  h->res_acc = h->acc_slot[0];  // the graph's kernels use the base (slot 0) buffers
+  h->res_sdraw = h->sdraw_slot[0];
   for (int64_t i = 0; i < n_iter; ++i) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
@@ -852,7 +955,7 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
   CUDA_TRY(cudaSetDevice(h->device));
   const size_t m = (size_t)h->c.m;
   uint8_t *st = h->result_stage;
-  if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->c.accepted, m, cudaMemcpyDeviceToHost, h->stream));
+  if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->res_acc, m, cudaMemcpyDeviceToHost, h->stream));
   if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + ((m + 7) & ~(size_t)7), h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   CUDA_TRY(cudaGetLastError());
@@ -863,7 +966,7 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
 
 int bart_get_accepted(bart_chain *h, uint8_t *out) {
   if (int rc = bart_sync(h)) return rc;
-  CUDA_TRY(cudaMemcpy(out, h->c.accepted, (size_t)h->c.m, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->res_acc, (size_t)h->c.m, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 
@@ -893,10 +996,7 @@ int bart_set_taps(bart_chain *h, int on) {
     CUDA_TRY(own(h, &c.tap_sums, (size_t)c.m * c.size));
   }
   c.taps = on ? 1 : 0;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 
@@ -908,10 +1008,7 @@ int bart_set_timeline(bart_chain *h, int on) {
   if (on && !h->trace_buf) CUDA_TRY(own(h, &h->trace_buf, (size_t)(c.m + 2) * c.nblk * 2));
   c.timeline = on ? h->timeline_buf : nullptr;
   c.trace = on ? h->trace_buf : nullptr;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
-  }
+  drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;
 }
 

@@ -297,6 +297,18 @@ class SamplerState:
         lo, hi = availability_intervals(self.forest, self.max_cuts)
         return (hi > lo).any(axis=2)
 
+    # -- results without waiting for the next step
+    def step_result(self, iteration: int | None = None) -> tuple[np.ndarray, float]:
+        """(last_accepted, sigma2) of step `iteration` (default: the latest) for
+        either of the last two `step` calls, from the pinned copy each step
+        enqueues behind itself: read step k after launching step k+1 and the
+        host's work for k+1 overlaps the device's step k."""
+        it = self.iteration - 1 if iteration is None else int(iteration)
+        a = np.empty(self._m, np.uint8)
+        v = np.empty(1, np.float64)
+        N.check(N.lib().bart_read_step_result(self._h, it, N.ptr(a), N.ptr(v)))
+        return a.astype(bool), float(v[0])
+
     # -- resume
     def restore(self, forest: Forest, leaf_index: np.ndarray, resid: np.ndarray, sigma2: float,
                 iteration: int) -> None:
