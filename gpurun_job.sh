@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'])"
-timeout 300 python tools/e2e_breakdown.py 1000000 100 2>&1 | tail -1
+timeout 200 python tools/timeline.py 100000 100 200 2>&1 | head -30
+timeout 200 python tools/timeline.py 1000000 100 200 2>&1 | head -8

@@ -257,7 +257,7 @@ struct APass {
 template <int W, int C, bool FIRST, bool TOTAL>
 __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
                                           const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
-                                          int warp, int lane, int base) {
+                                          int warp, int lane, int base, long long *ts = nullptr) {
   uint32_t sn[C > 0 ? C : 1];
   double acc[C > 0 ? C : 1];
   double tot = 0.0;
@@ -285,6 +285,7 @@ __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W
       }
     }
   }
+  TL_STAMP(ts && base == 0) ts[24] = gtimer_after(tot + (C > 0 ? acc[0] : 0.0));
   double rest = tot;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
@@ -295,13 +296,14 @@ __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W
   if (TOTAL) {  // slot ns-1 = total - others (per thread, then reduced)
     const double v = warp_sum_f64(rest);
     if (lane == 0) S.wsum[warp][A.ns - 1] = v;
+    TL_STAMP(ts) ts[25] = gtimer_after(v);
   }
 }
 
 template <int W>
 __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)[W], const uint32_t (&lc)[W],
                                             const APass &A, const Geom &G, const float *dlt, SweepSmem &S, int tid,
-                                            int warp, int lane) {
+                                            int warp, int lane, long long *ts = nullptr) {
   // compared-slot variants {0, 1, 2, 3} + the total for trees of <= 4 leaves;
   // wider trees take 8-slot passes.  Few variants: the control warp's code
   // must stay in the instruction cache next to the workers'.
@@ -319,23 +321,23 @@ __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)
     return;
   }
   switch (A.ns) {
-    case 1: sums_pass<W, 0, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 2: sums_pass<W, 1, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 3: sums_pass<W, 2, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 1: sums_pass<W, 0, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 2: sums_pass<W, 1, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 3: sums_pass<W, 2, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
 #ifndef BART_SUMS_WIDE_VARIANTS
 #define BART_SUMS_WIDE_VARIANTS 1
 #endif
 #if BART_SUMS_WIDE_VARIANTS
     // one variant per width: a compared slot costs ~300 cycles per pass
     // (tools/apass_bench.cu), more than the variants' instruction-cache cost
-    case 5: sums_pass<W, 4, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 6: sums_pass<W, 5, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 7: sums_pass<W, 6, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
-    case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+    case 5: sums_pass<W, 4, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 6: sums_pass<W, 5, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 7: sums_pass<W, 6, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
 #else
     case 5: case 6: case 7: case 8:
-      sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0); break;
+      sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
 #endif
     default:
       sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
@@ -991,9 +993,11 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
       A.gL = reinterpret_cast<uint32_t *>(c.L + (size_t)(e > 0 ? e - 1 : 0) * c.n_pad + G.start);
       A.slots = rec_hdr(G.rec(e)).slot_node;
       A.ns = G.hdr[e].nslots;
-      sums_passes<W>(r, lp, lc, A, G, S.dlt, S, tid, warp, lane);
+      long long *ts = tl ? tl + (size_t)(e + 1) * 32 : nullptr;
+      TL_STAMP(ts) ts[26] = gtimer_after((double)A.ns + (double)A.slots[0]);
+      sums_passes<W>(r, lp, lc, A, G, S.dlt, S, tid, warp, lane, ts);
 #if BART_TIMELINE
-      if (lane == 0 && G.cta == 0 && c.timeline) {  // every worker warp's A-pass end
+      if (lane == 0 && G.cta == 0 && c.timeline && warp < 8) {  // worker warps' A-pass ends (0-7)
         const volatile double dep = S.wsum[warp][0];
         (void)dep;
         c.timeline[(size_t)(e + 1) * 32 + 16 + warp] = gtimer();

@@ -47,7 +47,11 @@ print("worker: decision->A start     ", q(t[:, 0][1:] - t[:, 11][:-1]))
 print("  ctrl arrive -> worker sync ret", q(t[:, 3] - t[:, 11]))
 print("  worker sync ret -> A start    ", q(t[:, 0][1:] - t[:, 3][:-1]))
 print("  worker B done -> ctrl arrive  ", q(t[:, 11] - t[:, 2]))
-wa = t[:, 16:30]
+wa = t[:, 16:24]
+print("  A setup (flags, slots)       ", q(t[:, 26] - t[:, 0]))
+print("  A word loop (update + sums)  ", q(t[:, 24] - t[:, 26]))
+print("  A warp reductions            ", q(t[:, 25] - t[:, 24]))
+print("  A reductions -> published    ", q(t[:, 1] - t[:, 25]))
 print("A end spread over worker warps ", q(wa.max(1) - wa.min(1)))
 print("A start -> last warp A end     ", q(wa.max(1) - t[:, 0]))
 print("last warp A end -> ctrl synced ", q(t[:, 4] - wa.max(1)))
