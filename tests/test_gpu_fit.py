@@ -50,3 +50,23 @@ def test_fit_recovers_friedman_and_diagnostics_without_draws():
     pr = predict(tr, X[:100])
     np.testing.assert_allclose(pr.mean, tr.yhat_train_mean.mean(axis=0)[:100], rtol=1e-9, atol=1e-9)
     assert tr.sigma.shape == (2, 100) and np.all(tr.sigma > 0)
+
+
+def test_fit_matches_reference_golden():
+    """Whole-API parity: the reference's own fit() (regression.py:145-216, host
+    Philox streams) recorded in tests/golden/fit.npz, against fit(rng="host")
+    here: identical accept decisions in every chain and iteration, and the kept
+    draws to f32 rounding (the device sums in a different f64 order)."""
+    import os
+    from paper_2410_23244_b200.regression import FitConfig, fit
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "fit.npz"))
+    n_trees, n_burn, n_kept, n_chains, seed = (int(v) for v in d["cfg"])
+    cfg = FitConfig(n_trees=n_trees, n_burn=n_burn, n_kept=n_kept, n_chains=n_chains, seed=seed, rng="host",
+                    keep_train_draws=True)
+    for trace_mode in ("device", "host"):
+        tr = fit(d["X"], d["y"], FitConfig(**{**cfg.__dict__, "trace": trace_mode}), X_test=d["X_test"])
+        np.testing.assert_array_equal(tr.accepted, d["accepted"].astype(bool))
+        np.testing.assert_allclose(tr.sigma, d["sigma"], rtol=1e-5)
+        np.testing.assert_allclose(tr.yhat_train, d["yhat_train"], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(tr.yhat_test, d["yhat_test"], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(tr.mean_leaves, d["mean_leaves"], rtol=1e-12)
