@@ -1,2 +1,1 @@
-timeout 200 python tools/timeline.py 100000 100 200 2>&1 | head -30
-timeout 200 python tools/timeline.py 1000000 100 200 2>&1 | head -8
+timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'])"

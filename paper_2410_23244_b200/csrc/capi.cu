@@ -119,6 +119,7 @@ struct bart_chain {
               step_out_ready[2] = {nullptr, nullptr};
   bool update_sigma = true;
   cudaGraphExec_t graph_step[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][injected randoms]
+  int64_t slot_iter[2] = {-1, -1};  // which iteration each result slot holds
 };
 
 namespace {
@@ -328,30 +329,12 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   // one StepRandoms block (move_u | accept_u | leaf_z | chi2), so an injected
   // block is one host->device copy from the pinned staging buffer
   const size_t rwords = (size_t)c.m * 5 + (size_t)c.m + (size_t)c.m * c.size + 1;
-  double *rb1 = nullptr, *sd1 = nullptr;
-  uint8_t *acc1 = nullptr;
   OWN(rm, rwords);
-  OWN(rb1, rwords);
-  OWN(sd1, 1);
-  OWN(acc1, (size_t)c.m);
   if (e == cudaSuccess) {
     ra = rm + (size_t)c.m * 5;
     rz = ra + c.m;
     rc2 = rz + (size_t)c.m * c.size;
     h->rblock[0] = rm;
-    h->rblock[1] = rb1;
-    h->sdraw_slot[1] = sd1;
-    h->acc_slot[1] = acc1;
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaMallocHost(&h->rstage[k], rwords * 8);
-    if (e == cudaSuccess) e = cudaMallocHost(&h->result_stage, (size_t)c.m + 16);
-    if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * (((size_t)c.m + 7) / 8 * 8 + 8));
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
-      e = cudaEventCreateWithFlags(&h->copy_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
-    }
   }
   OWN(s2, 1);
   OWN(s2d, 1);
@@ -792,12 +775,36 @@ int bart_set_state(bart_chain *h, const uint16_t *axis, const uint8_t *cutpoint,
   return BART_OK;
 }
 
+// the bart_step pipeline's second slot, pinned stages, copy streams and
+// events, made on the first bart_step (device-RNG chains driven by bart_run,
+// like fit()'s, never pay for them)
+static cudaError_t ensure_step_pipeline(bart_chain *h) {
+  if (h->step_out) return cudaSuccess;
+  const ChainDev &c = h->c;
+  const size_t rwords = (size_t)c.m * 5 + (size_t)c.m + (size_t)c.m * c.size + 1;
+  cudaError_t e = own(h, &h->rblock[1], rwords);
+  if (e == cudaSuccess) e = own(h, &h->sdraw_slot[1], 1);
+  if (e == cudaSuccess) e = own(h, &h->acc_slot[1], (size_t)c.m);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaMallocHost(&h->rstage[k], rwords * 8);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&h->copy_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // the new buffers' zero fill
+  if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * (((size_t)c.m + 7) / 8 * 8 + 8));
+  return e;
+}
+
 int bart_step(bart_chain *h, const bart_randoms *rnd) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
   if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
+  CUDA_TRY(ensure_step_pipeline(h));
   const int slot = (int)(h->iteration & 1);
   ChainDev args = step_args(h, rnd ? 0 : 1);
   double *blk = h->rblock[slot];
@@ -848,12 +855,14 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   h->res_acc = h->acc_slot[slot];
   h->res_sdraw = h->sdraw_slot[slot];
   // this step's result -> pinned step_out[slot] on d2h, behind the step
+  const int64_t it = h->iteration - 1;
   const size_t stride = ((size_t)c.m + 7) / 8 * 8 + 8;
   uint8_t *dst = h->step_out + (size_t)slot * stride;
   CUDA_TRY(cudaStreamWaitEvent(h->d2h, h->kernel_done[slot], 0));
   CUDA_TRY(cudaMemcpyAsync(dst, h->acc_slot[slot], (size_t)c.m, cudaMemcpyDeviceToHost, h->d2h));
   CUDA_TRY(cudaMemcpyAsync(dst + stride - 8, h->sdraw_slot[slot], 8, cudaMemcpyDeviceToHost, h->d2h));
   CUDA_TRY(cudaEventRecord(h->step_out_ready[slot], h->d2h));
+  h->slot_iter[slot] = it;
   return BART_OK;
 }
 
@@ -861,6 +870,8 @@ int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, d
   if (!h) return fail(BART_EINVAL, "NULL handle");
   if (iteration < 0 || iteration < h->iteration - 2 || iteration >= h->iteration)
     return fail(BART_EINVAL, "only the last two bart_step results are kept");
+  if (!h->step_out || h->slot_iter[iteration & 1] != iteration)
+    return fail(BART_ESTATE, "iteration " + std::to_string(iteration) + " did not run through bart_step");
   CUDA_TRY(cudaSetDevice(h->device));
   CUDA_TRY(cudaEventSynchronize(h->step_out_ready[iteration & 1]));
   const size_t stride = ((size_t)h->c.m + 7) / 8 * 8 + 8;
@@ -893,7 +904,8 @@ int bart_run(bart_chain *h, int64_t n_iter) {
   CUDA_TRY(cudaSetDevice(h->device));
   if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   ensure_graph(h);
-  for (int k = 0; k < 2; ++k) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
+  for (int k = 0; k < 2; ++k)
+    if (h->step_out_ready[k]) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
   h->res_acc = h->acc_slot[0];  // the graph's kernels use the base (slot 0) buffers
   h->res_sdraw = h->sdraw_slot[0];
   for (int64_t i = 0; i < n_iter; ++i) {
@@ -954,6 +966,7 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   CUDA_TRY(cudaSetDevice(h->device));
   const size_t m = (size_t)h->c.m;
+  if (!h->result_stage) CUDA_TRY(cudaMallocHost(&h->result_stage, m + 16));
   uint8_t *st = h->result_stage;
   if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->res_acc, m, cudaMemcpyDeviceToHost, h->stream));
   if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + ((m + 7) & ~(size_t)7), h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
