@@ -288,6 +288,17 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   // mode (residuals in global memory / L2, refreshed rows in Lref)
   c.stream = sweep_words_per_thread(c.chunk) == 0 ? 1 : 0;
   if (const char *fs = getenv("BART_FORCE_STREAM")) c.stream |= atoi(fs) != 0;  // tests: stream mode at small n
+  c.persist_bytes = 0;
+  if (c.stream) {  // L2 set-aside for the residuals (stream mode's persisting window, sweep_launch)
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    size_t want = (size_t)4 * round16(c.n);
+    if (want > (size_t)max_window) want = (size_t)max_window;
+    if (want > (size_t)max_persist) want = (size_t)max_persist;
+    if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) c.persist_bytes = want;
+    cudaGetLastError();
+  }
   h->smem = sweep_smem_bytes(c.m, c.chunk, c.size, c.stream != 0);
   if ((int64_t)h->smem > optin)
     return bail(fail(BART_EINVAL, "sweep needs " + std::to_string(h->smem) + " B shared memory > " +

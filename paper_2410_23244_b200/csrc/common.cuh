@@ -121,6 +121,7 @@ struct ChainDev {
   uint64_t seed;
   int nblk, chunk;
   int stream;     // 1: chunk beyond the register budget -- residuals in global (L2) memory
+  size_t persist_bytes;  // stream mode: bytes of r in the launch's persisting L2 window (0: none)
   uint8_t *Lref;  // stream mode: (3, n_pad) refreshed larger-tree rows of trees e-1, e, e+1
   long long *timeline;        // optional per-tree phase stamps (clock64), CTA 0 and last CTA
   long long *trace;           // optional (m+1, nblk, 2) globaltimer: publish, gathered

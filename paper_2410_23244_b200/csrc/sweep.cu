@@ -1171,8 +1171,18 @@ __device__ __forceinline__ void stream_refresh_count(const ChainDev &c, const Ge
       l[k] = 0u;
       x[k] = 0u;
       if (w < G.nwords) {
-        l[k] = write ? L32[w] : O32[w];
-        if (write && g) x[k] = X32[w];
+#ifndef BART_STREAM_EVICT_FIRST
+#define BART_STREAM_EVICT_FIRST 1
+#endif
+        // the cache row and split column are read once per sweep: streaming
+        // loads, so they do not evict the L2-resident residuals and Lref rows
+        if (BART_STREAM_EVICT_FIRST) {
+          l[k] = write ? __ldcs(L32 + w) : O32[w];
+          if (write && g) x[k] = __ldcs(X32 + w);
+        } else {
+          l[k] = write ? L32[w] : O32[w];
+          if (write && g) x[k] = X32[w];
+        }
       }
     }
 #pragma unroll
@@ -1494,11 +1504,25 @@ int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s) {
   cfg.blockDim = dim3(kSweepThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+#ifndef BART_STREAM_PERSIST
+#define BART_STREAM_PERSIST 1
+#endif
+  if (BART_STREAM_PERSIST && c.stream && c.persist_bytes > 0) {
+    // stream mode: keep the residuals L2-resident (persisting window) while the
+    // cache rows and split columns stream past
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = c.r;
+    attr[1].val.accessPolicyWindow.num_bytes = c.persist_bytes;
+    attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
   return (int)cudaLaunchKernelEx(&cfg, sweep_fn(c.stream ? 0 : sweep_words_per_thread(c.chunk)), c);
 }
 
