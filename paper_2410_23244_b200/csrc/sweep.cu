@@ -61,7 +61,7 @@ constexpr int kCtrlWarp = kWorkWarps;  // then the helper warp
 // (DECISION).  Signals whose producer may run a tree ahead of its consumer
 // (counts -> helper, prep -> control, decision -> helper) are mbarriers with
 // one phase per tree and a buffer per tree parity.
-enum : int { BAR_PARTIALS = 1, BAR_DECISION = 2 };
+enum : int { BAR_PARTIALS = 1, BAR_DECISION = 2, BAR_ROLES = 3 };
 constexpr int kBarWC = kWorkers + 32;  // workers + control
 
 // count-only precomputation for one tree (see prepare())
@@ -973,7 +973,13 @@ __device__ __forceinline__ void worker_loop(const ChainDev &c, SweepSmem &S, con
     r[k] = w < G.nwords ? gr4[w] : make_float4(0.f, 0.f, 0.f, 0.f);
     lp[k] = lc[k] = ln[k] = 0u;
   }
-  __syncthreads();  // prologue barrier (mbarriers initialised, trees 0..3 in flight)
+  // role prologue barrier (mbarriers initialised, first trees in flight),
+  // reached by each warp role from its own code, as the per-tree named
+  // barriers are: warp-uniform, role-divergent bar.sync, the warp-specialised
+  // pattern of CUTLASS's NamedBarrier.  (The non-.aligned barrier.sync forms,
+  // which compute-sanitizer's synccheck accepts, measured 8% slower, and so
+  // did an mbarrier here: code layout.)
+  named_sync(BAR_ROLES, kSweepThreads);
   const int m = G.m;
   if (m > 0) {  // tree 0: refresh + counts
     mbar_wait(&S.mbar[0], 0u);
@@ -1219,7 +1225,7 @@ __device__ __forceinline__ void stream_refresh_count_all(const ChainDev &c, cons
 
 __device__ __forceinline__ void stream_worker_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int tid, int warp,
                                                    int lane) {
-  __syncthreads();  // prologue barrier
+  named_sync(BAR_ROLES, kSweepThreads);  // role prologue barrier
   const int m = G.m;
   if (m > 0) {
     mbar_wait(&S.mbar[0], 0u);
@@ -1283,7 +1289,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
                                              const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
   const XCtx X(c, G.cta);
-  __syncthreads();  // prologue barrier
+  named_sync(BAR_ROLES, kSweepThreads);  // role prologue barrier
   for (int e = 0; e <= m; ++e) {
     const bool has_cur = e < m;
     const TreeHdr hd = has_cur ? G.hdr[e] : TreeHdr{};
@@ -1369,7 +1375,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   };
   if (lane == 0)
     for (int j = 0; j < kRing && j < m; ++j) issue_tree(j);
-  __syncthreads();  // prologue barrier
+  named_sync(BAR_ROLES, kSweepThreads);  // role prologue barrier
   for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
     mbar_wait(&S.cnt_mbar[j & 1], par2(j));
     counts_add(c, X, S, j, G.hdr[j].nslots, lane);
