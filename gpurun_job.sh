@@ -1,3 +1,1 @@
-timeout 600 compute-sanitizer --tool memcheck python tools/sanitize_smoke.py 2>&1 | tail -1
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-timeout 600 python tools/variants.py bench v10 base v10 base -- --steps 200 --warmup 5 --e2e-steps 2
+timeout 1500 python tools/variants.py bench base pad1 pad2 pad3 pad4 pad5 pad6 pad7 base -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
