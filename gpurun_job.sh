@@ -1,1 +1,2 @@
-timeout 1500 python tools/variants.py bench base pad1 pad2 pad3 pad4 pad5 pad6 pad7 base -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(json.dumps(d['forest_kernels']))"

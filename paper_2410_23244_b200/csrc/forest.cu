@@ -178,6 +178,7 @@ __device__ __forceinline__ void valid_pts(uint32_t (&v)[K], int64_t i0, int64_t 
 }
 
 constexpr int kTravWords = 4;  // 16 points per thread (tools: 8 measured 20% slower at n = 1e6)
+constexpr int kTravTrees = 4;  // trees per traverse block (grid y)
 // leaf values staged in shared memory as f64, kLeafStage doubles per block
 // (the conversion once per leaf instead of once per point and tree)
 constexpr int kLeafStage = 4096;
@@ -191,7 +192,10 @@ __global__ void __launch_bounds__(256) traverse_kernel(const uint8_t *__restrict
   const int lane = threadIdx.x & 31;
   uint32_t v[K], l[K];
   valid_pts<K>(v, i0, n);
-  for (int j = 0; j < m; ++j) {
+  // blockIdx.y: a group of kTravTrees trees (independent outputs), so enough
+  // warps are in flight to cover the X column loads' latency
+  const int j0 = blockIdx.y * kTravTrees, j1 = j0 + kTravTrees < m ? j0 + kTravTrees : m;
+  for (int j = j0; j < j1; ++j) {
     traverse_pts<K>(l, Xt, ld, i0, live, cut + (size_t)j * half, axis + (size_t)j * half, half, lane);
     if (live) {
 #pragma unroll
@@ -206,7 +210,9 @@ static unsigned grid_for(int64_t ld, int words) { return (unsigned)((ld / (4 * w
 void launch_traverse(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, int m, const uint16_t *axis,
                      const uint8_t *cut, uint8_t *L, cudaStream_t s) {
   (void)D;
-  traverse_kernel<<<grid_for(ld, kTravWords), 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, L);
+  if (m <= 0) return;
+  const dim3 grid(grid_for(ld, kTravWords), (unsigned)((m + kTravTrees - 1) / kTravTrees));
+  traverse_kernel<<<grid, 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, L);
 }
 
 // trees [j0, j0 + nt) of the leaf table -> shared memory as f64 (whole block)
@@ -254,8 +260,42 @@ __global__ void __launch_bounds__(256) predict_cached_kernel(const uint8_t *__re
     if (w * 4 + b < n) out[w * 4 + b] = acc[b];
 }
 
+// Trees of <= 64 leaf slots (D <= 6): the warp holds the tree's leaf row in
+// registers (lane k: slots k and k + 32) and looks values up by shuffle
+// instead of gathering them through L1.
+__global__ void __launch_bounds__(256) predict_shfl_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m,
+                                                           int size, const float *__restrict__ leaf,
+                                                           double *__restrict__ out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = w * 4 < ld;
+  const int lane = threadIdx.x & 31;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int j = 0; j < m; ++j) {
+    const float *row = leaf + (size_t)j * size;
+    const float lo = lane < size ? __ldg(row + lane) : 0.f, hi = lane + 32 < size ? __ldg(row + lane + 32) : 0.f;
+    const uint32_t l = live ? __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w) : 0u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t h = (l >> (8 * b)) & 0xffu;
+      const float a = __shfl_sync(0xffffffffu, lo, h & 31u), c = __shfl_sync(0xffffffffu, hi, h & 31u);
+      acc[b] = __dadd_rn(acc[b], (double)(h < 32u ? a : c));
+    }
+  }
+  if (live)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (w * 4 + b < n) out[w * 4 + b] = acc[b];
+}
+
 void launch_predict_cached(const uint8_t *L, int64_t n, int64_t ld, int m, int size, const float *leaf,
                            double *out, cudaStream_t s) {
+#ifndef BART_PREDICT_SHFL
+#define BART_PREDICT_SHFL 1
+#endif
+  if (BART_PREDICT_SHFL && size <= 64) {
+    predict_shfl_kernel<<<grid_for(ld, 1), 256, 0, s>>>(L, n, ld, m, size, leaf, out);
+    return;
+  }
   predict_cached_kernel<<<grid_for(ld, 1), 256, 0, s>>>(L, n, ld, m, size, leaf, out);
 }
 
