@@ -1,2 +1,2 @@
-for i in 1 2 3; do timeout 300 python tools/fit_bench.py 1000 10 50 1 2>&1 | tail -2; done
-nproc; cat /proc/loadavg
+timeout 1500 python tools/variants.py bench v11 bo32 bo100 bo250 v11 -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
+timeout 900 python tools/variants.py bench v11 bo32 bo100 -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 --no-cpu
