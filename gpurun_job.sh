@@ -1,2 +1,5 @@
-timeout 1500 python tools/variants.py bench v11 bo32 bo100 bo250 v11 -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
-timeout 900 python tools/variants.py bench v11 bo32 bo100 -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 --no-cpu
+timeout 300 python tools/predict_bench.py 100000 200 200 2>&1 | tail -1
+BART_LIB=paper_2410_23244_b200/lib/variants/v11.so timeout 300 python tools/predict_bench.py 100000 200 200 2>&1 | tail -1
+timeout 300 python tools/predict_bench.py 1000000 50 200 2>&1 | tail -1
+timeout 300 python tools/predict_bench.py 10000 500 200 2>&1 | tail -1
+BART_LIB=paper_2410_23244_b200/lib/variants/v11.so timeout 300 python tools/predict_bench.py 10000 500 200 2>&1 | tail -1

@@ -1,6 +1,7 @@
 // C ABI (include/bart_b200.h): chain handles, host<->device layout changes,
 // step orchestration (propose kernel + persistent sweep, optionally replayed
 // from a CUDA graph), readback taps and measurement hooks.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1175,24 +1176,34 @@ int bart_evaluate_many(const bart_dims *dims, int64_t n_forests, const uint16_t 
   CUDA_TRY(cudaSetDevice(device));
   const int64_t n = dims->n, ld = round16(n);
   const int m = dims->m, D = dims->max_depth, half = 1 << (D - 1), size = 1 << D, p = dims->p;
+  // forests go up and are evaluated a batch at a time (one launch per batch,
+  // grid y = forest): enough forests to give the GPU ~4 blocks per SM when
+  // one forest's point tiles are fewer (small n); a batch's output <= 512 MB
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t tiles = (ld / 16 + 255) / 256;
+  const int64_t want = std::max<int64_t>(1, (4 * (int64_t)sms + tiles - 1) / tiles);
+  const int64_t batch = std::max<int64_t>(
+      1, std::min<int64_t>({n_forests, want, (512ll << 20) / std::max<int64_t>(1, n * 8), (int64_t)65535}));
   DevBuf xs, xt, da, dc, dl, pred;
   CUDA_TRY(xs.alloc((size_t)n * p));
   CUDA_TRY(xt.alloc((size_t)ld * p));
-  CUDA_TRY(da.alloc((size_t)m * half * 2));
-  CUDA_TRY(dc.alloc((size_t)m * half));
-  CUDA_TRY(dl.alloc((size_t)m * size * 4));
-  CUDA_TRY(pred.alloc((size_t)n * 8));
+  CUDA_TRY(da.alloc((size_t)batch * m * half * 2));
+  CUDA_TRY(dc.alloc((size_t)batch * m * half));
+  CUDA_TRY(dl.alloc((size_t)batch * m * size * 4));
+  CUDA_TRY(pred.alloc((size_t)batch * n * 8));
   CUDA_TRY(cudaMemset(xt.p, 0, (size_t)ld * p));
   CUDA_TRY(cudaMemcpy(xs.p, X, (size_t)n * p, cudaMemcpyHostToDevice));
   launch_transpose_u8(xs.as<uint8_t>(), n, p, p, xt.as<uint8_t>(), ld, 0);
-  for (int64_t f = 0; f < n_forests; ++f) {
-    CUDA_TRY(cudaMemcpy(da.p, axis + (size_t)f * m * half, (size_t)m * half * 2, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(dc.p, cutpoint + (size_t)f * m * half, (size_t)m * half, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(dl.p, leaf_value + (size_t)f * m * size, (size_t)m * size * 4, cudaMemcpyHostToDevice));
-    launch_evaluate(xt.as<uint8_t>(), n, ld, D, half, m, da.as<uint16_t>(), dc.as<uint8_t>(), dl.as<float>(),
-                    pred.as<double>(), 0);
+  for (int64_t f0 = 0; f0 < n_forests; f0 += batch) {
+    const int64_t nf = std::min<int64_t>(batch, n_forests - f0);
+    CUDA_TRY(cudaMemcpy(da.p, axis + (size_t)f0 * m * half, (size_t)nf * m * half * 2, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dc.p, cutpoint + (size_t)f0 * m * half, (size_t)nf * m * half, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dl.p, leaf_value + (size_t)f0 * m * size, (size_t)nf * m * size * 4, cudaMemcpyHostToDevice));
+    launch_evaluate_batch(xt.as<uint8_t>(), n, ld, D, half, m, (int)nf, da.as<uint16_t>(), dc.as<uint8_t>(),
+                          dl.as<float>(), pred.as<double>(), 0);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpy(out + (size_t)f * n, pred.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out + (size_t)f0 * n, pred.p, (size_t)nf * n * 8, cudaMemcpyDeviceToHost));
   }
   return BART_OK;
 }

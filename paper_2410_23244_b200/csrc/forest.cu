@@ -308,6 +308,13 @@ __global__ void __launch_bounds__(256) evaluate_kernel(const uint8_t *__restrict
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 * K;
   const bool live = i0 < ld;
   const int lane = threadIdx.x & 31, size = 2 * half;
+  // grid y: one forest of a stacked batch (forest f at axis/cut + f*m*half,
+  // leaf + f*m*size, out + f*n)
+  const size_t f = blockIdx.y;
+  axis += f * (size_t)m * half;
+  cut += f * (size_t)m * half;
+  leaf += f * (size_t)m * size;
+  out += f * (size_t)n;
   __shared__ double s_leaf[kLeafStage];
   double acc[4 * K];
 #pragma unroll
@@ -327,8 +334,15 @@ __global__ void __launch_bounds__(256) evaluate_kernel(const uint8_t *__restrict
 
 void launch_evaluate(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, int m, const uint16_t *axis,
                      const uint8_t *cut, const float *leaf, double *out, cudaStream_t s) {
+  launch_evaluate_batch(Xt, n, ld, D, half, m, 1, axis, cut, leaf, out, s);
+}
+
+void launch_evaluate_batch(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, int m, int n_forests,
+                           const uint16_t *axis, const uint8_t *cut, const float *leaf, double *out, cudaStream_t s) {
   (void)D;
-  evaluate_kernel<<<grid_for(ld, kTravWords), 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, leaf, out);
+  if (n_forests <= 0 || n <= 0) return;
+  const dim3 grid(grid_for(ld, kTravWords), (unsigned)n_forests);
+  evaluate_kernel<<<grid, 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, leaf, out);
 }
 
 // r = f32(f64(y) - pred)  (tests/util.py:19-23 recomputation)

@@ -25,6 +25,9 @@ void launch_predict_cached(const uint8_t *L, int64_t n, int64_t ld, int m, int s
                            double *out, cudaStream_t s);
 void launch_evaluate(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, int m, const uint16_t *axis,
                      const uint8_t *cut, const float *leaf, double *out, cudaStream_t s);
+// n_forests stacked forests (F, m, ...) evaluated at once (grid y = forest), out (F, n)
+void launch_evaluate_batch(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, int m, int n_forests,
+                           const uint16_t *axis, const uint8_t *cut, const float *leaf, double *out, cudaStream_t s);
 void launch_resid(const float *y, const double *pred, float *r, int64_t n, cudaStream_t s);
 void launch_trace_train(const uint8_t *L, int64_t n, int64_t ld, int m, int size, const float *leaf, int64_t k,
                         double *mean, double *m2, double *draw, double *pts, int npts, cudaStream_t s);
