@@ -15,8 +15,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("procs,n,trees,iters", [(2, 3000, 6, 3), (3, 7001, 8, 4)])
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
 def test_sharded_chain_over_processes(procs, n, trees, iters):
-    port = 29570 + procs
+    port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={procs}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tools", "ipc_shard_check.py"), str(n), str(trees), str(iters)]
