@@ -134,6 +134,31 @@ def test_forest_kernels_match_reference(case):
     np.testing.assert_array_equal(evaluate_forest(f, d["X"]), d["yhat"])
 
 
+@pytest.mark.parametrize("n,F", [(301, 37), (70001, 9)])
+def test_evaluate_forests_batches_match_single(n, F):
+    """Stacked forests evaluated a batch per launch (grid y = forest) equal one
+    evaluate_forest per forest, bit for bit, across batch boundaries; and the
+    tree-group traversal equals the cached sum (trees.py:206-223)."""
+    from paper_2410_23244_b200.sampler import Hyperparams, init_state, run, DeviceRNG
+    from paper_2410_23244_b200.trees import evaluate_forest, evaluate_forests, sum_leaf_values, traverse_forest
+    rng = np.random.default_rng(n)
+    p = 7
+    X = rng.integers(0, 30, (n, p)).astype(np.uint8)
+    y = rng.normal(size=n).astype(np.float32)
+    hp = Hyperparams(leaf_sd=0.3, lam=0.1, n_trees=13, max_depth=6)
+    st = init_state(X, np.full(p, 29), y, hp, DeviceRNG(5))
+    forests = []
+    for _ in range(F):
+        run(st, hp, 3)
+        forests.append(st.forest)
+    st.close()
+    got = evaluate_forests(forests, X)
+    for k in (0, F // 2, F - 1):
+        np.testing.assert_array_equal(got[k], evaluate_forest(forests[k], X))
+        L = traverse_forest(forests[k], X)
+        np.testing.assert_array_equal(sum_leaf_values(forests[k].leaf_value, L), got[k])
+
+
 @pytest.fixture(params=["register", "stream"])
 def sweep_mode(request, monkeypatch):
     """Run a test in both sweep modes: register-resident points (the default at
