@@ -263,13 +263,12 @@ __global__ void __launch_bounds__(256) predict_cached_kernel(const uint8_t *__re
 // Trees of <= 64 leaf slots (D <= 6): the warp holds the tree's leaf row in
 // registers (lane k: slots k and k + 32) and looks values up by shuffle
 // instead of gathering them through L1.
-__global__ void __launch_bounds__(256) predict_shfl_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m,
-                                                           int size, const float *__restrict__ leaf,
-                                                           double *__restrict__ out) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = w * 4 < ld;
-  const int lane = threadIdx.x & 31;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+// sum over trees (ascending, f64) of the 4 points of cache word w; leaf rows
+// of <= 64 slots, looked up by shuffle (the whole warp must call it)
+__device__ __forceinline__ void sum_trees_shfl(double (&acc)[4], const uint8_t *__restrict__ L, int64_t ld, int64_t w,
+                                               bool live, int m, int size, const float *__restrict__ leaf, int lane) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) acc[b] = 0.0;
   for (int j = 0; j < m; ++j) {
     const float *row = leaf + (size_t)j * size;
     const float lo = lane < size ? __ldg(row + lane) : 0.f, hi = lane + 32 < size ? __ldg(row + lane + 32) : 0.f;
@@ -281,6 +280,15 @@ __global__ void __launch_bounds__(256) predict_shfl_kernel(const uint8_t *__rest
       acc[b] = __dadd_rn(acc[b], (double)(h < 32u ? a : c));
     }
   }
+}
+
+__global__ void __launch_bounds__(256) predict_shfl_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m,
+                                                           int size, const float *__restrict__ leaf,
+                                                           double *__restrict__ out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = w * 4 < ld;
+  double acc[4];
+  sum_trees_shfl(acc, L, ld, w, live, m, size, leaf, threadIdx.x & 31);
   if (live)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
@@ -370,14 +378,19 @@ __global__ void __launch_bounds__(256) trace_train_kernel(const uint8_t *__restr
                                                           double *__restrict__ draw, double *__restrict__ pts,
                                                           int npts) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w * 4 >= ld) return;
+  const bool live = w * 4 < ld;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int j = 0; j < m; ++j) {
-    const uint32_t l = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w);
-    const float *row = leaf + (size_t)j * size;
+  if (size <= 64) {  // block-uniform
+    sum_trees_shfl(acc, L, ld, w, live, m, size, leaf, threadIdx.x & 31);
+  } else if (live) {
+    for (int j = 0; j < m; ++j) {
+      const uint32_t l = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w);
+      const float *row = leaf + (size_t)j * size;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
+      for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
+    }
   }
+  if (!live) return;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int64_t i = w * 4 + b;

@@ -14,7 +14,6 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("procs,n,trees,iters", [(2, 3000, 6, 3), (3, 7001, 8, 4)])
 def _free_port() -> int:
     import socket
     with socket.socket() as sock:
@@ -22,6 +21,7 @@ def _free_port() -> int:
         return sock.getsockname()[1]
 
 
+@pytest.mark.parametrize("procs,n,trees,iters", [(2, 3000, 6, 3), (3, 7001, 8, 4)])
 def test_sharded_chain_over_processes(procs, n, trees, iters):
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={procs}",
