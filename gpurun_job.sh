@@ -1,1 +1,5 @@
-timeout 900 ncu --set full --clock-control none -k regex:traverse_kernel -s 2 -c 1 -o gpurun_out/traverse_full python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu > gpurun_out/ncu_trav.log 2>&1; tail -1 gpurun_out/ncu_trav.log
+timeout 300 python bench.py --no-cpu --steps 100 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('before ref', d['value'], d['e2e']['value'])"
+timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > /dev/null 2>&1
+timeout 300 python bench.py --no-cpu --steps 100 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('after ref', d['value'], d['e2e']['value'])"
+timeout 300 python tools/fit_bench.py 1000 10 50 1 2>&1 | tail -2
+ps aux --sort=-%cpu | head -5
