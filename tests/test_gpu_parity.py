@@ -298,3 +298,34 @@ def test_unconnected_shard_refuses_to_step():
     with pytest.raises(ValueError):
         st.shard_connect([st.shard_export()])  # one handle for two shards
     st.close()
+
+
+def test_pipelined_step_results_match_synchronous_reads():
+    """state.step_result(k), read after step k+1 was launched (the e2e loop),
+    equals what a synchronous read right after step k returns."""
+    from paper_2410_23244_b200.sampler import Hyperparams, StepRandoms, init_state, step
+    rng = np.random.default_rng(11)
+    n, p, m = 2500, 5, 9
+    X = rng.integers(0, 12, (n, p)).astype(np.uint8)
+    y = rng.normal(size=n).astype(np.float32)
+    hp = Hyperparams(leaf_sd=0.3, lam=0.1, n_trees=m, max_depth=5)
+    blocks = [StepRandoms.draw(rng, m, 32, hp.nu + n) for _ in range(8)]
+    a = init_state(X, np.full(p, 11), y, hp, None, sigma2=1.0)
+    want = []
+    for rnd in blocks:
+        step(a, hp, randoms=rnd)
+        want.append((a.last_accepted.copy(), a.sigma2))
+    b = init_state(X, np.full(p, 11), y, hp, None, sigma2=1.0)
+    got = []
+    for k, rnd in enumerate(blocks):
+        step(b, hp, randoms=rnd)
+        if k > 0:
+            got.append(b.step_result(b.iteration - 2))
+    got.append(b.step_result())
+    for (wa, ws), (ga, gs) in zip(want, got):
+        np.testing.assert_array_equal(wa, ga)
+        assert ws == gs
+    with pytest.raises(ValueError):
+        b.step_result(0)  # only the last two steps are kept
+    a.close()
+    b.close()
