@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(json.dumps({k:(v['ms'] if isinstance(v,dict) else v) for k,v in d['forest_kernels'].items()}))"
-BART_LIB=paper_2410_23244_b200/lib/variants/fk0.so timeout 300 python bench.py --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(json.dumps({k:(v['ms'] if isinstance(v,dict) else v) for k,v in d['forest_kernels'].items()}))"
+timeout 900 env BART_LIB=paper_2410_23244_b200/lib/variants/roles.so python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+timeout 900 python tools/variants.py bench v12 roles v12 roles -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
+timeout 900 python tools/variants.py bench v12 roles -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 --no-cpu
