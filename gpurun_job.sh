@@ -1,3 +1,8 @@
-timeout 900 env BART_LIB=paper_2410_23244_b200/lib/variants/roles.so python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
-timeout 900 python tools/variants.py bench v12 roles v12 roles -- --steps 200 --warmup 5 --e2e-steps 2 --no-cpu
-timeout 900 python tools/variants.py bench v12 roles -- --n 100000 --steps 300 --warmup 5 --e2e-steps 2 --no-cpu
+# Round validation on one B200 (run through gpurun): GPU tests, the bench line,
+# the reference arm, the ncu launch list and full capture of the sweep.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
+timeout 300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json | cut -c1-200
+timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2>/dev/null
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --e2e-steps 2 --no-cpu > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep -s 3 -c 1 -o gpurun_out/sweep_full python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu > gpurun_out/ncu_full.log 2>&1
