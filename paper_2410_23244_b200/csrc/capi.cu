@@ -144,6 +144,8 @@ void free_chain(bart_chain *h) {
   for (void *p : h->owned)
     if (p) cudaFree(p);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  // a stream-mode chain pinned its residuals in L2: release the persisting lines
+  if (h->c.persist_bytes > 0) cudaCtxResetPersistingL2Cache();
   if (h->h2d) cudaStreamSynchronize(h->h2d);
   if (h->d2h) cudaStreamSynchronize(h->d2h);
   for (auto *p : h->rstage)
