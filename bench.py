@@ -4,7 +4,11 @@
 Workload (default, BASELINE configs[2], the metric's config): gbart on
 synthetic Friedman #1 data, n=1e6, p=100, ntree=200, D=6, 100 uniform
 cutpoints.  A "step" is one full MCMC iteration (propose + sequential sweep
-over all 200 trees + sigma draw) on resident device state.
+over all 200 trees + sigma draw) on resident device state.  The chain is
+burned in (--burn, default 200 iterations, like the reference protocol's
+warm-up, bench.py:114-122) before the W warm-up and K timed steps, so the
+number is a steady-state one (trees at their posterior size, reported as
+"trees" in the line), not the 1-2-leaf trees of a fresh chain.
 
   value     iterations/s of CUDA-graph-replayed device-RNG steps, CUDA events
             on the chain's stream, max over ranks; inputs (X 100 MB, leaf
@@ -15,12 +19,13 @@ over all 200 trees + sigma draw) on resident device state.
             last_accepted + sigma2 every step.
   roofline  the sweep kernel: algorithmic bytes 10*n*m per launch (SURVEY.md
             §8d) / mean per-launch CUDA-event duration, vs measured HBM peak.
-  cpu_baseline  the CPU oracle (numpy port of the reference, oracle/) on a
-            bounded sample: full n and p, 10 trees, scaled to 200 trees.
+  cpu_baseline  the CPU oracle (numpy port of the reference, oracle/), one
+            core, full workload (n, p, all 200 trees): 1 warm-up + 3 timed
+            steps, median.
 
 `--impl reference` times the CPU oracle port with all host cores
-(independent chains, one per core) on the same workload and prints the same
-JSON line with "impl": "reference".
+(independent chains, one per core, each running full 200-tree steps) on the
+same workload and prints the same JSON line with "impl": "reference".
 """
 
 from __future__ import annotations
@@ -41,7 +46,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MCMC iters/sec at n=1e6,p=100,ntree=200 (1/2/4/8 B200) vs host CPU; HBM GB/s"
-CPU_SAMPLE_TREES = 10
+CPU_TIMED_STEPS = 3  # per chain, after one warm-up step: full-workload iterations
+REF_MAX_STEPS = 8    # reference arm: timed steps actually run (each ~3 s at n=1e6)
 
 
 def parse():
@@ -49,13 +55,15 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--burn", type=int, default=200,
+                    help="iterations run before warm-up so the timed chain is at steady state")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--p", type=int, default=100)
     ap.add_argument("--m", type=int, default=200)
     ap.add_argument("--depth", type=int, default=6)
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=CPU_TIMED_STEPS)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--shard", action="store_true",
@@ -73,10 +81,26 @@ def workload(args):
     return Xq, grid.counts, ys.forward(y).astype(np.float32), hp
 
 
+def baseline_config_label(args) -> str:
+    """Which BASELINE.json config this workload is."""
+    shape = (args.n, args.p, args.m)
+    if shape == (100_000, 100, 200):
+        return "BASELINE.json configs[1]"
+    if shape == (1_000_000, 100, 200):
+        return "BASELINE.json configs[2]"
+    if shape == (10_000_000, 100, 200):
+        return "BASELINE.json configs[3]"
+    if shape == (1_000_000, 1000, 1000):
+        return "BASELINE.json configs[4]"
+    if shape == (1000, 10, 50):
+        return "BASELINE.json configs[0] shape"
+    return "not a BASELINE.json config"
+
+
 def config_dict(args, parallelism):
     return {
         "workload": f"gbart Friedman#1 n={args.n:g} p={args.p} ntree={args.m} D={args.depth} "
-                    f"(BASELINE.json configs[2])",
+                    f"({baseline_config_label(args)})",
         "n": args.n, "p": args.p, "ntree": args.m, "max_depth": args.depth, "n_cutpoints": 100,
         "parallelism": parallelism,
         "l2": "no flush: X (n*p B) + leaf index (n*m B) per iteration exceed the 126 MB L2",
@@ -142,27 +166,29 @@ def committed_traffic():
 
 # ---------------------------------------------------------------- CPU side
 def _cpu_worker(args_tuple):
-    Xq, max_cuts, y32, hp_fields, m_sample, steps, seed = args_tuple
+    """One CPU chain of the full workload: `warm` untimed then `steps` timed
+    full iterations (all m trees) of the oracle port; per-step seconds."""
+    Xq, max_cuts, y32, hp_fields, warm, steps, seed = args_tuple
     from types import SimpleNamespace
 
     from oracle.bart_oracle import OracleChain
 
     hp = SimpleNamespace(**hp_fields)
-    hp.n_trees = m_sample
+    m = hp.n_trees
     ch = OracleChain(Xq, max_cuts, y32, hp)
     rng = np.random.default_rng(seed)
     size = 1 << hp.max_depth
     times = []
-    for s in range(steps + 1):  # first step is warm-up
-        u = rng.random((m_sample, 5))
-        acc = rng.random(m_sample)
-        z = rng.standard_normal((m_sample, size))
+    for s in range(warm + steps):
+        u = rng.random((m, 5))
+        acc = rng.random(m)
+        z = rng.standard_normal((m, size))
         chi2 = float(rng.chisquare(hp.nu + y32.size))
         t0 = time.perf_counter()
         ch.step(u, acc, z, chi2)
-        if s > 0:
+        if s >= warm:
             times.append(time.perf_counter() - t0)
-    return statistics.median(times)
+    return times
 
 
 def _hp_fields(hp):
@@ -171,19 +197,26 @@ def _hp_fields(hp):
                 update_sigma=hp.update_sigma)
 
 
-def cpu_oracle_rate(Xq, max_cuts, y32, hp, m_full, steps, procs=1):
-    """Per-chain iters/s of the oracle, sampled with CPU_SAMPLE_TREES trees and scaled to m_full."""
-    job = (Xq, max_cuts, y32, _hp_fields(hp), CPU_SAMPLE_TREES, steps)
+def cpu_oracle_times(Xq, max_cuts, y32, hp, warm, steps, procs=1):
+    """Per-step seconds of `procs` concurrent oracle chains of the full
+    workload (one process per chain), each `warm` + `steps` iterations."""
+    job = (Xq, max_cuts, y32, _hp_fields(hp), warm, steps)
     if procs <= 1:
-        t = _cpu_worker(job + (0,))
-        per_chain = [t]
-    else:
-        ctx = mp.get_context("fork")
-        with ctx.Pool(procs) as pool:
-            per_chain = pool.map(_cpu_worker, [job + (k,) for k in range(procs)])
-    scale = m_full / CPU_SAMPLE_TREES
-    rates = [1.0 / (t * scale) for t in per_chain]
-    return sum(rates), per_chain
+        return [_cpu_worker(job + (0,))]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        return pool.map(_cpu_worker, [job + (k,) for k in range(procs)])
+
+
+def tree_stats(st) -> dict:
+    """Leaves per tree of the chain's forest at the start of the timed region
+    (a leaf-less heap slot has cutpoint 0: trees.py:174-203)."""
+    f = st.forest
+    leaves = (f.cutpoint > 0).sum(axis=1) + 1
+    hist = np.bincount(leaves, minlength=leaves.max() + 1)
+    return {"mean_leaves": float(leaves.mean()), "max_leaves": int(leaves.max()),
+            "leaves_hist": {str(k): int(v) for k, v in enumerate(hist) if v},
+            "iteration": int(st.iteration)}
 
 
 # ---------------------------------------------------------------- GPU side
@@ -263,6 +296,9 @@ def run_ours(args):
         # replicas: every rank runs an independent chain of the full workload
         st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local)
     cfg = st.sweep_config()
+    run(st, hp, args.burn)  # to steady state (trees at posterior size)
+    st.sync()
+    trees = tree_stats(st)
     run(st, hp, args.warmup)
     st.sync()
     launches0 = st.kernel_launches()
@@ -315,11 +351,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        rate, per = cpu_oracle_rate(Xq, max_cuts, y32, hp, args.m, args.cpu_steps, procs=1)
-        cpu = {"value": rate, "unit": "iters/s", "cores": 1, "kind": "port",
-               "sample": f"oracle/bart_oracle.py (numpy port of bforge.sampler.step) at n={args.n}, p={args.p} "
-                         f"with {CPU_SAMPLE_TREES} trees, median of {args.cpu_steps} steps "
-                         f"({statistics.median(per):.2f} s), scaled x{args.m // CPU_SAMPLE_TREES} to {args.m} trees"}
+        (times,) = cpu_oracle_times(Xq, max_cuts, y32, hp, 1, args.cpu_steps, procs=1)
+        med = statistics.median(times)
+        cpu = {"value": 1.0 / med, "unit": "iters/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/bart_oracle.py (numpy port of bforge.sampler.step), the full workload "
+                         f"(n={args.n}, p={args.p}, all {args.m} trees): 1 warm-up + {len(times)} timed "
+                         f"iterations of one chain on one core, median {med:.2f} s"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -349,6 +386,8 @@ def run_ours(args):
             "gpu_launches": gpu_launches,
             "cuda_graph": graph,
             "sweep_grid": cfg,
+            "burn_in": args.burn,
+            "trees": trees,
             "clocks": clk.summary(),
             "forest_kernels": forest_kernels,
         }
@@ -360,24 +399,31 @@ def run_ours(args):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle port (the reference is pure Python and
+    cannot travel to the GPU box) on every host core, one independent chain of
+    the FULL workload per core.  Each step is one full m-tree iteration of
+    every chain; min(K, REF_MAX_STEPS) timed steps after min(W, 1) warm-up
+    (each step takes seconds), all reported as run."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     Xq, max_cuts, y32, hp = workload(args)
-    procs = os.cpu_count() or 1
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = min(args.warmup, 1)
     t0 = time.perf_counter()
-    rates = []
-    for _ in range(max(1, args.steps if args.steps <= 3 else 1)):
-        rate, per = cpu_oracle_rate(Xq, max_cuts, y32, hp, args.m, args.cpu_steps, procs=procs)
-        rates.append(rate)
+    per_chain = cpu_oracle_times(Xq, max_cuts, y32, hp, warm, steps, procs=procs)
     wall = time.perf_counter() - t0
-    value = statistics.median(rates)
+    # chains run concurrently: step k of the job takes the slowest chain's step k
+    step_s = [max(t[k] for t in per_chain) for k in range(steps)]
+    ms_per_step = 1e3 * statistics.fmean(step_s)
+    value = procs * 1e3 / ms_per_step
     sample = (f"oracle port (numpy restatement of bforge.sampler.step; the reference is pure Python and is not "
-              f"buildable) at n={args.n}, p={args.p}: {procs} independent chains (one per core), each "
-              f"{CPU_SAMPLE_TREES} trees x {args.cpu_steps} steps, per-tree time scaled to {args.m} trees")
+              f"buildable) at n={args.n}, p={args.p}, ntree={args.m}: {procs} independent chains (one process per "
+              f"core), each {warm} warm-up + {steps} timed full iterations; job step = slowest chain's step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value * procs,
+        "steps": steps, "steps_requested": args.steps, "warmup": warm, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 resid / f64 sums",
         "data": "synthetic Friedman #1 (binned uint8)", "config": config_dict(args, f"{procs} CPU chains"),
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": procs, "kind": "port", "sample": sample},

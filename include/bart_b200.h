@@ -15,7 +15,8 @@
  * Errors: every function returns BART_OK (0) or a status code; the message of
  * the last failure on the calling thread is returned by bart_last_error().
  * BART_EINVAL maps to the reference's ValueError (shape/config checks,
- * sampler.py:214-217, trees.py:63-67), BART_ECUDA / BART_ESTATE to RuntimeError.
+ * sampler.py:214-217, trees.py:63-67), BART_ECUDA / BART_ESTATE / BART_ERANGE to
+ * RuntimeError.
  * Threading: one writer per handle; handles are independent.
  */
 #ifndef BART_B200_H
@@ -31,6 +32,12 @@ extern "C" {
 #define BART_EINVAL 1
 #define BART_ECUDA 2
 #define BART_ESTATE 3
+/* The step's cross-CTA exchange met a non-finite value or one outside its
+ * exact fixed-point range (per-CTA partial >= 2^46 / CTAs, e.g. an
+ * unstandardised y with sum(r^2) ~ 1e14, or a NaN residual).  Sticky: the
+ * chain's state is no longer the reference's; every later call that syncs
+ * returns it until bart_set_state resets the chain. */
+#define BART_ERANGE 4
 
 #define BART_MAX_DEPTH 8 /* trees.py:27-28: leaf heap index fits one byte */
 

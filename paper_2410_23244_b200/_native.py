@@ -15,7 +15,7 @@ import numpy as np
 
 from ._build import LIB
 
-BART_OK, BART_EINVAL, BART_ECUDA, BART_ESTATE = 0, 1, 2, 3
+BART_OK, BART_EINVAL, BART_ECUDA, BART_ESTATE, BART_ERANGE = 0, 1, 2, 3, 4
 MAX_DEPTH = 8
 SHARD_HANDLE_BYTES = 256
 PROPOSAL_ROWS = 12

@@ -48,6 +48,11 @@ struct DevBuf {  // scoped temporary device buffer
 
 int64_t round16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
+constexpr const char *kRangeMsg =
+    "the step's exchange met a NaN/inf or a per-CTA partial outside its exact fixed-point range "
+    "(|partial| < 2^46 / CTAs; e.g. an unstandardised y whose sum of squared residuals exceeds ~1e11 "
+    "per SM, or a non-finite residual): the chain state is invalid; reset it with set_state";
+
 int check_dims(const bart_dims *d) {
   if (!d) return fail(BART_EINVAL, "dims is NULL");
   if (d->max_depth < 1 || d->max_depth > BART_MAX_DEPTH)
@@ -784,14 +789,28 @@ int bart_set_state(bart_chain *h, const uint16_t *axis, const uint8_t *cutpoint,
     CUDA_TRY(cudaStreamSynchronize(s));
   }
   if (sigma2 >= 0.0) CUDA_TRY(cudaMemcpyAsync(c.sigma2, &sigma2, 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(c.err, 0, sizeof(int), s));  // a reset chain is valid again (BART_ERANGE)
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaGetLastError());
+  return BART_OK;
+}
+
+// The sweep's sticky exchange-range flag (sweep.cu to_limbs), read after the
+// stream has synchronised.
+static int check_range(bart_chain *h) {
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, h->c.err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) return fail(BART_ERANGE, kRangeMsg);
   return BART_OK;
 }
 
 // the bart_step pipeline's second slot, pinned stages, copy streams and
 // events, made on the first bart_step (device-RNG chains driven by bart_run,
 // like fit()'s, never pay for them)
+// one bart_step result in pinned memory: accept flags (m, padded to 8) |
+// sigma2 draw (8 B) | exchange error flag (8 B)
+static size_t step_out_stride(int m) { return ((size_t)m + 7) / 8 * 8 + 16; }
+
 static cudaError_t ensure_step_pipeline(bart_chain *h) {
   if (h->step_out) return cudaSuccess;
   const ChainDev &c = h->c;
@@ -808,7 +827,7 @@ static cudaError_t ensure_step_pipeline(bart_chain *h) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // the new buffers' zero fill
-  if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * (((size_t)c.m + 7) / 8 * 8 + 8));
+  if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * step_out_stride(c.m));
   return e;
 }
 
@@ -870,11 +889,12 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   h->res_sdraw = h->sdraw_slot[slot];
   // this step's result -> pinned step_out[slot] on d2h, behind the step
   const int64_t it = h->iteration - 1;
-  const size_t stride = ((size_t)c.m + 7) / 8 * 8 + 8;
+  const size_t stride = step_out_stride(c.m);
   uint8_t *dst = h->step_out + (size_t)slot * stride;
   CUDA_TRY(cudaStreamWaitEvent(h->d2h, h->kernel_done[slot], 0));
   CUDA_TRY(cudaMemcpyAsync(dst, h->acc_slot[slot], (size_t)c.m, cudaMemcpyDeviceToHost, h->d2h));
-  CUDA_TRY(cudaMemcpyAsync(dst + stride - 8, h->sdraw_slot[slot], 8, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(cudaMemcpyAsync(dst + stride - 16, h->sdraw_slot[slot], 8, cudaMemcpyDeviceToHost, h->d2h));
+  CUDA_TRY(cudaMemcpyAsync(dst + stride - 8, c.err, 4, cudaMemcpyDeviceToHost, h->d2h));
   CUDA_TRY(cudaEventRecord(h->step_out_ready[slot], h->d2h));
   h->slot_iter[slot] = it;
   return BART_OK;
@@ -888,12 +908,15 @@ int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, d
     return fail(BART_ESTATE, "iteration " + std::to_string(iteration) + " did not run through bart_step");
   CUDA_TRY(cudaSetDevice(h->device));
   CUDA_TRY(cudaEventSynchronize(h->step_out_ready[iteration & 1]));
-  const size_t stride = ((size_t)h->c.m + 7) / 8 * 8 + 8;
+  const size_t stride = step_out_stride(h->c.m);
   const uint8_t *src = h->step_out + (size_t)(iteration & 1) * stride;
+  int err = 0;
+  std::memcpy(&err, src + stride - 8, 4);
+  if (err) return fail(BART_ERANGE, kRangeMsg);
   if (accepted) std::memcpy(accepted, src, (size_t)h->c.m);
   if (sigma2) {
     if (h->update_sigma) {
-      std::memcpy(sigma2, src + stride - 8, 8);  // the step's draw became sigma2 (sampler.py:906-908)
+      std::memcpy(sigma2, src + stride - 16, 8);  // the step's draw became sigma2 (sampler.py:906-908)
     } else {  // sigma2 is not sampled: the (unchanged) state value
       CUDA_TRY(cudaMemcpy(sigma2, h->c.sigma2, 8, cudaMemcpyDeviceToHost));
     }
@@ -940,7 +963,7 @@ int bart_sync(bart_chain *h) {
   CUDA_TRY(cudaSetDevice(h->device));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   CUDA_TRY(cudaGetLastError());
-  return BART_OK;
+  return check_range(h);
 }
 
 int bart_get_forest(bart_chain *h, uint16_t *axis, uint8_t *cutpoint, float *leaf_value) {
@@ -980,14 +1003,19 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   CUDA_TRY(cudaSetDevice(h->device));
   const size_t m = (size_t)h->c.m;
-  if (!h->result_stage) CUDA_TRY(cudaMallocHost(&h->result_stage, m + 16));
+  if (!h->result_stage) CUDA_TRY(cudaMallocHost(&h->result_stage, m + 24));
   uint8_t *st = h->result_stage;
+  const size_t m8 = (m + 7) & ~(size_t)7;
   if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->res_acc, m, cudaMemcpyDeviceToHost, h->stream));
-  if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + ((m + 7) & ~(size_t)7), h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
+  if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + m8, h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaMemcpyAsync(st + m8 + 8, h->c.err, 4, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   CUDA_TRY(cudaGetLastError());
+  int err = 0;
+  std::memcpy(&err, st + m8 + 8, 4);
+  if (err) return fail(BART_ERANGE, kRangeMsg);
   if (accepted) std::memcpy(accepted, st, m);
-  if (sigma2) std::memcpy(sigma2, st + ((m + 7) & ~(size_t)7), 8);
+  if (sigma2) std::memcpy(sigma2, st + m8, 8);
   return BART_OK;
 }
 
@@ -1257,7 +1285,7 @@ int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
   CUDA_TRY(cudaEventElapsedTime(ms, a, b));
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  return BART_OK;
+  return check_range(h);
 }
 
 int bart_graph_active(bart_chain *h) { return h && h->graph ? 1 : 0; }
@@ -1328,7 +1356,7 @@ int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
   ms[0] = tot;
   ms[1] = sw;
   ms[2] = pr;
-  return BART_OK;
+  return check_range(h);
 }
 
 }  // extern "C"

@@ -434,9 +434,13 @@ __device__ __forceinline__ void refresh_count(uint32_t (&out)[W], const uint8_t 
 
 // ------------------------------------------------------------ exchange
 // f64 -> 111-bit two's-complement fixed point with 64 fraction bits, as three
-// 37-bit limbs.  Exact for 2^-12 <= |x| < 2^45; tinier values round at 2^-64.
-__device__ __forceinline__ void to_limbs(double x, unsigned long long (&l)[3], int *err) {
-  if (!(fabs(x) < 0x1.0p45)) {  // also catches NaN
+// 37-bit limbs.  Exact for 2^-12 <= |x| < lim; tinier values round at 2^-64.
+// lim = 2^46 / (CTAs over all shards, rounded up to a power of two), so the
+// sum of every CTA's partial stays below 2^46 and never wraps the 111-bit
+// total.  A partial outside it (or NaN) sets the chain's sticky error flag,
+// which the host turns into BART_ERANGE at the next sync (capi.cu).
+__device__ __forceinline__ void to_limbs(double x, unsigned long long (&l)[3], int *err, double lim) {
+  if (!(fabs(x) < lim)) {  // also catches NaN
     if (err) atomicOr(err, 1);
     x = 0.0;
   }
@@ -489,16 +493,24 @@ __device__ __forceinline__ int pin_int(int v) {
   asm volatile("" : "+r"(v));
   return v;
 }
+// 2^46 / (ctas rounded up to a power of two): the per-CTA bound of to_limbs
+__device__ __forceinline__ double xrange_limit(int ctas) {
+  int bits = 0;
+  while ((1 << bits) < ctas) ++bits;
+  return ldexp(1.0, 46 - bits);
+}
 struct XCtx {
   unsigned long long *xacc, *cacc;
   int *err;
   int n_shards, nblk_total;
   bool sys;
+  double lim;  // per-CTA fixed-point range (to_limbs)
   // xacc/cacc: the copy this CTA polls
   __device__ __forceinline__ XCtx(const ChainDev &c, int cta)
       : xacc(pin_ptr(c.copy_groups > 1 ? c.xpeer[c.copy_base + cta % c.copy_groups] : c.xacc)),
         cacc(pin_ptr(c.copy_groups > 1 ? c.cpeer[c.copy_base + cta % c.copy_groups] : c.cacc)), err(pin_ptr(c.err)),
-        n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0) {}
+        n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0),
+        lim(xrange_limit(c.nblk_total)) {}
 };
 
 // Control warp, exchange X: fold the worker warps' f64 partials of ns slots
@@ -527,7 +539,7 @@ __device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx &X, c
         for (int k = 0; k + step < kWorkWarps; k += 2 * step) w[k] = __dadd_rn(w[k], w[k + step]);
       TL_STAMP(ts && s0 == 0) ts[14] = gtimer_after(w[0]);
       unsigned long long l[3];
-      to_limbs(w[0], l, X.err);
+      to_limbs(w[0], l, X.err, X.lim);
       TL_STAMP(ts && s0 == 0) ts[15] = gtimer_after(__longlong_as_double((long long)(l[2] | l[1] | l[0])));
       if (q < 3) {
         const unsigned long long v = kTagOne | pick3(l, q);

@@ -21,7 +21,10 @@ Xq = rng.integers(0, 101, (n, p), dtype=np.uint8)
 y = 10 * np.sin(np.pi * Xq[:, 0] * Xq[:, 1] / 1e4) + 20 * (Xq[:, 2] / 100 - .5) ** 2 + 10 * Xq[:, 3] / 100 + rng.normal(size=n)
 hp, ys = derive_hyperparams(y, FitConfig(n_trees=m))
 st = init_state(Xq, np.full(p, 100), ys.forward(y).astype(np.float32), hp, DeviceRNG(1))
-run(st, hp, 20); st.sync()
+burn = int(os.environ.get("BART_TL_BURN", "20"))
+run(st, hp, burn); st.sync()
+lv = (st.forest.cutpoint > 0).sum(axis=1) + 1
+print(f"burn-in {burn} iterations: mean leaves/tree {lv.mean():.2f}, max {lv.max()}")
 N.check(N.lib().bart_set_timeline(st.handle, 1))
 ms = np.zeros(3, np.float32)
 N.check(N.lib().bart_profile(st.handle, 3, N.ptr(ms)))
@@ -40,8 +43,7 @@ print("  red issued -> add loop exit  ", q(t[:, 5] - t[:, 30]))
 print("adds -> prep loaded           ", q(t[:, 6] - t[:, 5]))
 print("prep -> poll complete         ", q(t[:, 7] - t[:, 6]))
 print("poll -> totals (gather/limbs) ", q(t[:, 8] - t[:, 7]))
-print("decide: division              ", q(t[:, 9] - t[:, 8]))
-print("decide: accept known          ", q(t[:, 10] - t[:, 9]))
+print("decide: poll -> accept known   ", q(t[:, 10] - t[:, 8]))
 print("decide: deltas + arrive       ", q(t[:, 11] - t[:, 10]))
 print("worker: decision->A start     ", q(t[:, 0][1:] - t[:, 11][:-1]))
 print("  ctrl arrive -> worker sync ret", q(t[:, 3] - t[:, 11]))
