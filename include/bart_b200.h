@@ -147,6 +147,14 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2);
  * (and draw its randoms on the host meanwhile) before reading step k. */
 int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, double *sigma2);
 int bart_get_proposals(bart_chain *h, int64_t *rows /* (12, m) */, double *struct_log /* (m,) */);
+/* The StepRandoms block (sampler.py:244-260 layout) the latest step consumed:
+ * the injected one, or the one drawn on the device from Philox4x32-10.  Any
+ * pointer may be NULL.  move_u (m,5), accept_u (m,), leaf_z (m,2^D), chi2 (1). */
+int bart_get_randoms(bart_chain *h, double *move_u, double *accept_u, double *leaf_z, double *chi2);
+/* Test hook: the device Philox4x32-10 bijection of the step (Random123's
+ * philox4x32_10) on `count` explicit (counter, key) pairs: ctr (count,4),
+ * key (count,2), out (count,4), uint32.  For known-answer tests. */
+int bart_philox4x32_10(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t count, int device);
 /* Phase taps for parity (enable with bart_set_taps before the step):
  * counts (m, 2^D) after the grow refresh (sampler.py:894-897) and the
  * tree-excluded sums (m, 2^D) each tree resolved with (sampler.py:828). */

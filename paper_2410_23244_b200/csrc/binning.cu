@@ -66,6 +66,7 @@ __global__ void quantize_kernel(const double *__restrict__ X, int64_t total, int
   const double *c = cuts + off[a];
   int hi = (int)(off[a + 1] - off[a]);  // count of cutpoints <= v, in [0, hi]
   int lo = 0;
+  if (v != v) lo = hi;  // NaN sorts after every cutpoint (np.searchsorted side="right", grid.py:127-128)
   while (lo < hi) {  // first index with c[idx] > v
     const int mid = (lo + hi) >> 1;
     if (__ldg(c + mid) <= v)

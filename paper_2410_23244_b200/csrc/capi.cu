@@ -119,6 +119,7 @@ struct bart_chain {
   double *sdraw_slot[2] = {nullptr, nullptr};
   uint8_t *res_acc = nullptr;  // where the latest step's accept flags are
   double *res_sdraw = nullptr;
+  double *res_block = nullptr;  // the random block (StepRandoms) the latest step consumed
   uint8_t *step_out = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, kernel_done[2] = {nullptr, nullptr},
@@ -389,6 +390,7 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   h->sdraw_slot[0] = s2d;
   h->res_acc = acc;
   h->res_sdraw = s2d;
+  h->res_block = rm;
   h->update_sigma = hp->update_sigma != 0;
   c.xacc = xacc;
   c.xpeer[0] = xacc;
@@ -887,6 +889,7 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   CUDA_TRY(cudaEventRecord(h->kernel_done[slot], h->stream));
   h->res_acc = h->acc_slot[slot];
   h->res_sdraw = h->sdraw_slot[slot];
+  h->res_block = blk;
   // this step's result -> pinned step_out[slot] on d2h, behind the step
   const int64_t it = h->iteration - 1;
   const size_t stride = step_out_stride(c.m);
@@ -945,6 +948,7 @@ int bart_run(bart_chain *h, int64_t n_iter) {
     if (h->step_out_ready[k]) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
   h->res_acc = h->acc_slot[0];  // the graph's kernels use the base (slot 0) buffers
   h->res_sdraw = h->sdraw_slot[0];
+  h->res_block = h->rblock[0];
   for (int64_t i = 0; i < n_iter; ++i) {
     if (h->graph) {
       CUDA_TRY(cudaGraphLaunch(h->graph, h->stream));
@@ -1022,6 +1026,35 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
 int bart_get_accepted(bart_chain *h, uint8_t *out) {
   if (int rc = bart_sync(h)) return rc;
   CUDA_TRY(cudaMemcpy(out, h->res_acc, (size_t)h->c.m, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_get_randoms(bart_chain *h, double *move_u, double *accept_u, double *leaf_z, double *chi2) {
+  if (int rc = bart_sync(h)) return rc;
+  const ChainDev &c = h->c;
+  const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
+  const double *b = h->res_block;
+  if (move_u) CUDA_TRY(cudaMemcpy(move_u, b, nm * 8, cudaMemcpyDeviceToHost));
+  if (accept_u) CUDA_TRY(cudaMemcpy(accept_u, b + nm, na * 8, cudaMemcpyDeviceToHost));
+  if (leaf_z) CUDA_TRY(cudaMemcpy(leaf_z, b + nm + na, nz * 8, cudaMemcpyDeviceToHost));
+  if (chi2) CUDA_TRY(cudaMemcpy(chi2, b + nm + na + nz, 8, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
+int bart_philox4x32_10(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t count, int device) {
+  if (!ctr || !key || !out || count < 0) return fail(BART_EINVAL, "bad philox arguments");
+  if (count == 0) return BART_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  DevBuf dc, dk, dout;
+  CUDA_TRY(dc.alloc((size_t)count * 16));
+  CUDA_TRY(dk.alloc((size_t)count * 8));
+  CUDA_TRY(dout.alloc((size_t)count * 16));
+  CUDA_TRY(cudaMemcpy(dc.p, ctr, (size_t)count * 16, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dk.p, key, (size_t)count * 8, cudaMemcpyHostToDevice));
+  launch_philox(dc.as<uint32_t>(), dk.as<uint32_t>(), dout.as<uint32_t>(), count, 0);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, dout.p, (size_t)count * 16, cudaMemcpyDeviceToHost));
   return BART_OK;
 }
 

@@ -37,4 +37,17 @@ void launch_propose(const ChainDev &c, int device_rng, cudaStream_t s) {
   propose_kernel<<<blocks, kProposeWarps * 32, 0, s>>>(c, device_rng);
 }
 
+__global__ void philox_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int64_t count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = philox(ctr[i], key[i]);
+}
+
+void launch_philox(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t count, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t blocks = (count + threads - 1) / threads;
+  philox_kernel<<<(unsigned)blocks, threads, 0, s>>>(reinterpret_cast<const uint4 *>(ctr),
+                                                    reinterpret_cast<const uint2 *>(key),
+                                                    reinterpret_cast<uint4 *>(out), count);
+}
+
 }  // namespace bart

@@ -382,6 +382,15 @@ class SamplerState:
         N.check(N.lib().bart_get_taps(self._h, N.ptr(cnt), N.ptr(sums)))
         return cnt, sums
 
+    def last_randoms(self) -> "StepRandoms":
+        """The StepRandoms block (sampler.py:244-260) the latest step consumed:
+        the injected one, or the one the device drew from Philox4x32-10."""
+        m, size = self._m, heap_size(self._D)
+        mu, au = np.empty((m, 5)), np.empty(m)
+        z, c2 = np.empty((m, size)), np.empty(1)
+        N.check(N.lib().bart_get_randoms(self._h, N.ptr(mu), N.ptr(au), N.ptr(z), N.ptr(c2)))
+        return StepRandoms(mu, au, z, float(c2[0]))
+
     def predict_train(self) -> np.ndarray:
         """trees.sum_leaf_values(forest.leaf_value, leaf_index) from the device cache."""
         out = np.empty(self.y.size, np.float64)
@@ -494,6 +503,18 @@ def init_state(X: np.ndarray, max_cuts: np.ndarray, y: np.ndarray, hp: Hyperpara
     if sigma2 is None:
         sigma2 = float(np.var(y32, ddof=1)) if n >= 2 else 1.0
     return SamplerState(X, max_cuts, y32, hp, rng, float(sigma2), device, max_ctas=max_ctas)
+
+
+def philox4x32_10(ctr: np.ndarray, key: np.ndarray, device: int = 0) -> np.ndarray:
+    """The device RNG's Philox4x32-10 bijection (Random123 philox4x32_10) on
+    explicit counters (k, 4) and keys (k, 2), uint32 -> (k, 4) uint32."""
+    ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+    key = np.ascontiguousarray(key, np.uint32).reshape(-1, 2)
+    if ctr.shape[0] != key.shape[0]:
+        raise ValueError("one key per counter")
+    out = np.empty_like(ctr)
+    N.check(N.lib().bart_philox4x32_10(N.ptr(ctr), N.ptr(key), N.ptr(out), ctr.shape[0], int(device)))
+    return out
 
 
 def _randoms_struct(rnd: StepRandoms):

@@ -36,3 +36,34 @@ def test_uniform_grid_ranges_on_device():
     with pytest.raises(ValueError):
         X[7, 1] = np.nan
         build_grid_uniform(X, 100, device=0)
+
+
+def _golden(name):
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
+
+
+def test_device_binning_matches_reference_golden():
+    """tests/golden/grid.npz was written by the reference's own
+    build_grid_uniform / build_grid_midpoints / quantize (make_golden.py):
+    the device min/max grid and device quantize reproduce it exactly."""
+    from paper_2410_23244_b200.grid import CutpointGrid, build_grid_uniform, quantize
+    g = _golden("grid.npz")
+    gu = build_grid_uniform(g["X"], 40, device=0)
+    np.testing.assert_array_equal(gu.counts, g["uniform_counts"])
+    np.testing.assert_array_equal(np.concatenate(gu.cutpoints), g["uniform_cuts"])
+    np.testing.assert_array_equal(quantize(g["X"], gu, device=0).data, g["q_train"])
+    np.testing.assert_array_equal(quantize(g["X_new"], gu, device=0).data, g["q_new"])
+    off = np.concatenate([[0], np.cumsum(g["mid_counts"])])
+    gm = CutpointGrid([g["mid_cuts"][off[a]:off[a + 1]] for a in range(len(g["mid_counts"]))])
+    np.testing.assert_array_equal(quantize(g["Xm"], gm, device=0).data, g["qm"])
+
+
+def test_device_quantize_non_finite_rows_match_reference():
+    """NaN -> len(cuts), +inf -> len(cuts), -inf -> 0, as the reference's
+    np.searchsorted(side="right") (grid.py:121-134; grid_special.npz)."""
+    from paper_2410_23244_b200.grid import CutpointGrid, quantize
+    g = _golden("grid_special.npz")
+    off = np.concatenate([[0], np.cumsum(g["counts"])])
+    grid = CutpointGrid([g["cuts"][off[a]:off[a + 1]] for a in range(len(g["counts"]))])
+    np.testing.assert_array_equal(quantize(g["X_special"], grid, device=0).data, g["q_special"])
