@@ -141,6 +141,15 @@ __device__ __forceinline__ void vstore(uint8_t *p, const uint32_t (&w)[K]) {
 
 // Leaf indices (bytes of l) of the thread's 4K points in tree j.  Every lane
 // of the warp must call it (ballot / shuffle); lanes past the row read nothing.
+// The internal nodes are taken kNodeBatch at a time: all their X column loads
+// are issued before the first SWAR step, so a tree of several internal nodes
+// waits for one memory latency instead of one per node (heap order, hence the
+// reference's descent, is kept: nodes are applied in ascending index).
+#ifndef BART_NODE_BATCH
+#define BART_NODE_BATCH 1
+#endif
+constexpr int kNodeBatch = BART_NODE_BATCH;
+
 template <int K>
 __device__ __forceinline__ void traverse_pts(uint32_t (&l)[K], const uint8_t *__restrict__ Xt, int64_t ld, int64_t i0,
                                              bool live, const uint8_t *__restrict__ cut_j,
@@ -151,17 +160,30 @@ __device__ __forceinline__ void traverse_pts(uint32_t (&l)[K], const uint8_t *__
     const int t = base + lane;
     const uint32_t ct = t < half ? __ldg(cut_j + t) : 0u, at = t < half ? __ldg(ax_j + t) : 0u;
     uint32_t msk = __ballot_sync(0xffffffffu, ct != 0u && t >= 1);
-    while (msk) {
-      const int src = __ffs(msk) - 1;
-      msk &= msk - 1u;
-      const uint32_t node = (uint32_t)(base + src);
-      const uint32_t cv = __shfl_sync(0xffffffffu, ct, src), av = __shfl_sync(0xffffffffu, at, src);
-      if (live) {
-        uint32_t x[K];
-        vload<K>(x, Xt + (size_t)av * ld + i0);
-        const uint32_t t4 = 0x01010101u * node, c4 = 0x01010101u * cv, b4 = 0x01010101u * (2u * node);
+    while (msk) {  // warp-uniform
+      uint32_t x[kNodeBatch][K], node[kNodeBatch], cv[kNodeBatch];
+      bool use[kNodeBatch];
 #pragma unroll
-        for (int k = 0; k < K; ++k) l[k] = swar_step(l[k], x[k], t4, c4, b4);
+      for (int g = 0; g < kNodeBatch; ++g) {
+        use[g] = msk != 0u;
+        node[g] = 0u;
+        cv[g] = 0u;
+        if (use[g]) {
+          const int src = __ffs(msk) - 1;
+          msk &= msk - 1u;
+          node[g] = (uint32_t)(base + src);
+          cv[g] = __shfl_sync(0xffffffffu, ct, src);
+          const uint32_t av = __shfl_sync(0xffffffffu, at, src);
+          if (live) vload<K>(x[g], Xt + (size_t)av * ld + i0);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kNodeBatch; ++g) {
+        if (use[g] && live) {
+          const uint32_t t4 = 0x01010101u * node[g], c4 = 0x01010101u * cv[g], b4 = 0x01010101u * (2u * node[g]);
+#pragma unroll
+          for (int k = 0; k < K; ++k) l[k] = swar_step(l[k], x[g][k], t4, c4, b4);
+        }
       }
     }
   }
@@ -178,6 +200,10 @@ __device__ __forceinline__ void valid_pts(uint32_t (&v)[K], int64_t i0, int64_t 
 }
 
 constexpr int kTravWords = 4;  // 16 points per thread (tools: 8 measured 20% slower at n = 1e6)
+#ifndef BART_EVAL_WORDS
+#define BART_EVAL_WORDS 4
+#endif
+constexpr int kEvalWords = BART_EVAL_WORDS;  // fused evaluate: words (4 points) per thread
 constexpr int kTravTrees = 4;  // trees per traverse block (grid y)
 // leaf values staged in shared memory as f64, kLeafStage doubles per block
 // (the conversion once per leaf instead of once per point and tree)
@@ -239,6 +265,30 @@ __device__ __forceinline__ void store_pts(double *__restrict__ out, int64_t i0, 
     if (i0 + b < n) out[i0 + b] = acc[b];
 }
 
+// the same sum for rows wider than 64 slots (D = 7, 8): leaf values gathered
+// through L1, kSumUnroll trees' cache words in flight per thread
+__device__ __forceinline__ void sum_trees_gather(double (&acc)[4], const uint8_t *__restrict__ L, int64_t ld, int64_t w,
+                                                 int m, int size, const float *__restrict__ leaf) {
+  int j = 0;
+  for (; j + 8 <= m; j += 8) {
+    uint32_t l[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) l[u] = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)(j + u) * ld) + w);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float *row = leaf + (size_t)(j + u) * size;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l[u] >> (8 * b)) & 0xffu)));
+    }
+  }
+  for (; j < m; ++j) {
+    const uint32_t l = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w);
+    const float *row = leaf + (size_t)j * size;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
+  }
+}
+
 // yhat[i] = sum_j leaf[j, L[j, i]] accumulated in f64, j ascending.  Four
 // points per thread, leaf values gathered through L1: at n = 1e6 this beat
 // 16 points per thread (206 us vs 136 us) and shared-memory f64 leaf tables
@@ -249,12 +299,7 @@ __global__ void __launch_bounds__(256) predict_cached_kernel(const uint8_t *__re
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w * 4 >= ld) return;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int j = 0; j < m; ++j) {
-    const uint32_t l = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w);
-    const float *row = leaf + (size_t)j * size;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
-  }
+  sum_trees_gather(acc, L, ld, w, m, size, leaf);
 #pragma unroll
   for (int b = 0; b < 4; ++b)
     if (w * 4 + b < n) out[w * 4 + b] = acc[b];
@@ -264,22 +309,145 @@ __global__ void __launch_bounds__(256) predict_cached_kernel(const uint8_t *__re
 // registers (lane k: slots k and k + 32) and looks values up by shuffle
 // instead of gathering them through L1.
 // sum over trees (ascending, f64) of the 4 points of cache word w; leaf rows
-// of <= 64 slots, looked up by shuffle (the whole warp must call it)
+// of <= 64 slots, looked up by shuffle (the whole warp must call it).
+// kSumUnroll trees' cache words and leaf rows are loaded before any of them is
+// used, so each warp keeps kSumUnroll independent row loads in flight (the
+// loop is bound by memory latency, not by the shuffles: one 128 B load per
+// warp and tree would leave HBM mostly idle).  The upper half of a row
+// (heap slots 32..63, leaves at depth 5) is shuffled only when a lane of the
+// warp indexes it -- rarely, trees are shallow.
+#ifndef BART_SUM_UNROLL
+#define BART_SUM_UNROLL 8
+#endif
+constexpr int kSumUnroll = BART_SUM_UNROLL;
+
+template <int U>
+__device__ __forceinline__ void sum_trees_block(double (&acc)[4], const uint32_t *__restrict__ Lw, int64_t ldw,
+                                                bool live, const float *__restrict__ lrow, int size, int lane) {
+  uint32_t l[U];
+  float lo[U], hi[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    lo[u] = lane < size ? __ldg(lrow + u * size) : 0.f;
+    hi[u] = lane + 32 < size ? __ldg(lrow + u * size + 32) : 0.f;
+    l[u] = live ? __ldg(Lw) : 0u;
+    Lw += ldw;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    // each lane widens its own leaf slot(s) once per tree, and the points
+    // fetch f64 values by shuffle: the f32->f64 conversion runs on the XU
+    // pipe, which a conversion per point and tree saturates (ncu)
+    const double dlo = (double)lo[u];
+    if (!__any_sync(0xffffffffu, (l[u] & 0xe0e0e0e0u) != 0u)) {  // no index >= 32 in the warp (shallow tree)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        acc[b] = __dadd_rn(acc[b], __shfl_sync(0xffffffffu, dlo, (l[u] >> (8 * b)) & 31u));
+    } else {
+      const double dhi = (double)hi[u];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t h = (l[u] >> (8 * b)) & 0xffu;
+        const double a = __shfl_sync(0xffffffffu, dlo, h & 31u), c = __shfl_sync(0xffffffffu, dhi, h & 31u);
+        acc[b] = __dadd_rn(acc[b], h < 32u ? a : c);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void sum_trees_shfl(double (&acc)[4], const uint8_t *__restrict__ L, int64_t ld, int64_t w,
                                                bool live, int m, int size, const float *__restrict__ leaf, int lane) {
 #pragma unroll
   for (int b = 0; b < 4; ++b) acc[b] = 0.0;
-  for (int j = 0; j < m; ++j) {
-    const float *row = leaf + (size_t)j * size;
-    const float lo = lane < size ? __ldg(row + lane) : 0.f, hi = lane + 32 < size ? __ldg(row + lane + 32) : 0.f;
-    const uint32_t l = live ? __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w) : 0u;
+  const int64_t ldw = ld / 4;  // cache row stride in words
+  const uint32_t *Lw = reinterpret_cast<const uint32_t *>(L) + w;
+  const float *lrow = leaf + lane;
+  int j = 0;
+  for (; j + kSumUnroll <= m; j += kSumUnroll) {
+    sum_trees_block<kSumUnroll>(acc, Lw, ldw, live, lrow, size, lane);
+    Lw += kSumUnroll * ldw;
+    lrow += kSumUnroll * size;
+  }
+  for (; j < m; ++j) {
+    sum_trees_block<1>(acc, Lw, ldw, live, lrow, size, lane);
+    Lw += ldw;
+    lrow += size;
+  }
+}
+
+// f64 leaf table in shared memory: every kSTrees trees the block widens the
+// trees' leaf rows to f64 once (one conversion per leaf value and block,
+// instead of one per point and tree on the slow XU conversion pipe), then each
+// point's lookup is one shared-memory gather of the f64 value.  Cache words
+// are loaded kSumUnroll trees ahead (memory-level parallelism).
+constexpr int kSTrees = 32;
+#ifndef BART_SMEM64_UNROLL
+#define BART_SMEM64_UNROLL 8
+#endif
+constexpr int kS64Unroll = BART_SMEM64_UNROLL;
+template <int SIZE, int P>
+__device__ __forceinline__ void sum_trees_smem64(double (&acc)[4 * P], const uint8_t *__restrict__ L, int64_t ld,
+                                                 int64_t w, bool live, int m, const float *__restrict__ leaf,
+                                                 double *s_tab) {
+  // P cache words (4P points) per thread: word w*P+p
+  typedef typename Vec<P>::T VT;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t h = (l >> (8 * b)) & 0xffu;
-      const float a = __shfl_sync(0xffffffffu, lo, h & 31u), c = __shfl_sync(0xffffffffu, hi, h & 31u);
-      acc[b] = __dadd_rn(acc[b], (double)(h < 32u ? a : c));
+  for (int b = 0; b < 4 * P; ++b) acc[b] = 0.0;
+  const int64_t ldv = ld / (4 * P);
+  const VT *Lv = reinterpret_cast<const VT *>(L) + w;
+  for (int j0 = 0; j0 < m; j0 += kSTrees) {
+    const int nt = m - j0 < kSTrees ? m - j0 : kSTrees;
+    __syncthreads();  // the previous chunk's table is consumed
+    for (int i = threadIdx.x; i < nt * SIZE; i += blockDim.x) s_tab[i] = (double)__ldg(leaf + (size_t)j0 * SIZE + i);
+    __syncthreads();
+    if (!live) continue;
+    int jj = 0;
+    for (; jj + kS64Unroll <= nt; jj += kS64Unroll) {
+      uint32_t l[kS64Unroll][P];
+#pragma unroll
+      for (int u = 0; u < kS64Unroll; ++u) {
+        const VT v = __ldg(Lv + (size_t)(j0 + jj + u) * ldv);
+        memcpy(l[u], &v, sizeof(VT));
+      }
+#pragma unroll
+      for (int u = 0; u < kS64Unroll; ++u) {
+        const double *row = s_tab + (jj + u) * SIZE;
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[4 * p + b] = __dadd_rn(acc[4 * p + b], row[(l[u][p] >> (8 * b)) & 0xffu]);
+      }
+    }
+    for (; jj < nt; ++jj) {
+      uint32_t l[P];
+      const VT v = __ldg(Lv + (size_t)(j0 + jj) * ldv);
+      memcpy(l, &v, sizeof(VT));
+      const double *row = s_tab + jj * SIZE;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[4 * p + b] = __dadd_rn(acc[4 * p + b], row[(l[p] >> (8 * b)) & 0xffu]);
     }
   }
+}
+
+#ifndef BART_SMEM64_WORDS
+#define BART_SMEM64_WORDS 1
+#endif
+constexpr int kS64Words = BART_SMEM64_WORDS;
+
+__global__ void __launch_bounds__(256) predict_smem64_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m,
+                                                             const float *__restrict__ leaf, double *__restrict__ out) {
+  constexpr int P = kS64Words;
+  __shared__ double s_tab[kSTrees * 64];
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = w * 4 * P < ld;
+  double acc[4 * P];
+  sum_trees_smem64<64, P>(acc, L, ld, w, live, m, leaf, s_tab);
+  if (live)
+#pragma unroll
+    for (int b = 0; b < 4 * P; ++b)
+      if (w * 4 * P + b < n) out[w * 4 * P + b] = acc[b];
 }
 
 __global__ void __launch_bounds__(256) predict_shfl_kernel(const uint8_t *__restrict__ L, int64_t n, int64_t ld, int m,
@@ -300,6 +468,13 @@ void launch_predict_cached(const uint8_t *L, int64_t n, int64_t ld, int m, int s
 #ifndef BART_PREDICT_SHFL
 #define BART_PREDICT_SHFL 1
 #endif
+#ifndef BART_PREDICT_SMEM64
+#define BART_PREDICT_SMEM64 1
+#endif
+  if (BART_PREDICT_SMEM64 && size == 64) {
+    predict_smem64_kernel<<<grid_for(ld, kS64Words), 256, 0, s>>>(L, n, ld, m, leaf, out);
+    return;
+  }
   if (BART_PREDICT_SHFL && size <= 64) {
     predict_shfl_kernel<<<grid_for(ld, 1), 256, 0, s>>>(L, n, ld, m, size, leaf, out);
     return;
@@ -312,7 +487,7 @@ __global__ void __launch_bounds__(256) evaluate_kernel(const uint8_t *__restrict
                                                        int m, const uint16_t *__restrict__ axis,
                                                        const uint8_t *__restrict__ cut,
                                                        const float *__restrict__ leaf, double *__restrict__ out) {
-  constexpr int K = kTravWords;
+  constexpr int K = kEvalWords;
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 * K;
   const bool live = i0 < ld;
   const int lane = threadIdx.x & 31, size = 2 * half;
@@ -349,7 +524,7 @@ void launch_evaluate_batch(const uint8_t *Xt, int64_t n, int64_t ld, int D, int 
                            const uint16_t *axis, const uint8_t *cut, const float *leaf, double *out, cudaStream_t s) {
   (void)D;
   if (n_forests <= 0 || n <= 0) return;
-  const dim3 grid(grid_for(ld, kTravWords), (unsigned)n_forests);
+  const dim3 grid(grid_for(ld, kEvalWords), (unsigned)n_forests);
   evaluate_kernel<<<grid, 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, leaf, out);
 }
 
@@ -380,15 +555,13 @@ __global__ void __launch_bounds__(256) trace_train_kernel(const uint8_t *__restr
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = w * 4 < ld;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (size <= 64) {  // block-uniform
+  __shared__ double s_tab[kSTrees * 64];
+  if (size == 64) {  // block-uniform (D = 6, the default depth)
+    sum_trees_smem64<64, 1>(acc, L, ld, w, live, m, leaf, s_tab);
+  } else if (size < 64) {
     sum_trees_shfl(acc, L, ld, w, live, m, size, leaf, threadIdx.x & 31);
   } else if (live) {
-    for (int j = 0; j < m; ++j) {
-      const uint32_t l = __ldg(reinterpret_cast<const uint32_t *>(L + (size_t)j * ld) + w);
-      const float *row = leaf + (size_t)j * size;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[b] = __dadd_rn(acc[b], (double)__ldg(row + ((l >> (8 * b)) & 0xffu)));
-    }
+    sum_trees_gather(acc, L, ld, w, m, size, leaf);
   }
   if (!live) return;
 #pragma unroll
