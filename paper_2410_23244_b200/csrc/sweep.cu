@@ -220,6 +220,39 @@ struct APass {
   int ns;
 };
 
+// Warp sums of V per-thread values at once, by transpose reduction: at each
+// butterfly level a lane keeps half of its values and trades the other half
+// with its partner (lanes L, L^bit), so V values cost ~V + log2(32) shuffle
+// rounds instead of 5V.  Every addition pairs the same lane groups as a
+// shfl_down tree (only the operand order differs, and IEEE addition is
+// commutative), so each total is bit-identical to warp_sum_f64's.  On return
+// the lane holds the total of value `idx`; lanes equal outside
+// xreduce_group_mask(V) hold the same total.
+template <int N, int BIT>
+__device__ __forceinline__ double warp_xreduce(const double (&a)[N], int lane, int &idx) {
+  if constexpr (N == 1) {
+    double x = a[0];
+#pragma unroll
+    for (int b = BIT; b >= 0; --b) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 1 << b));
+    return x;
+  } else {
+    constexpr int H = (N + 1) / 2, R = N - H;
+    const bool up = (lane >> BIT) & 1;
+    double keep[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      const double lo = a[k], hi = k < R ? a[H + k] : 0.0;
+      const double mine = up ? hi : lo, other = up ? lo : hi;
+      keep[k] = __dadd_rn(mine, __shfl_xor_sync(0xffffffffu, other, 1 << BIT));
+    }
+    if (up) idx += H;
+    return warp_xreduce<H, BIT - 1>(keep, lane, idx);
+  }
+}
+// lanes sharing one total: the bits below the last halving level
+__host__ __device__ constexpr int xreduce_levels(int n) { return n <= 1 ? 0 : 1 + xreduce_levels((n + 1) / 2); }
+__host__ __device__ constexpr int xreduce_group_mask(int n) { return (1 << (5 - xreduce_levels(n))) - 1; }
+
 // A pass over the register-resident chunk.  FIRST: tree e-1's update
 // (residuals f32 with the reference's two roundings, sampler.py:755-760;
 // cache write of the final tree).  Then the f64 residual sums of tree e over
@@ -259,17 +292,24 @@ __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W
     }
   }
   TL_STAMP(ts && base == 0) ts[24] = gtimer_after(tot + (C > 0 ? acc[0] : 0.0));
+  // the C compared slots, then (TOTAL) slot ns-1 = total - others per thread
+  constexpr int V = C + (TOTAL ? 1 : 0);
+  double vals[V > 0 ? V : 1];
   double rest = tot;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
-    const double v = warp_sum_f64(acc[s]);
+    vals[s] = acc[s];
     if (TOTAL) rest = __dsub_rn(rest, acc[s]);
-    if (lane == 0 && base + s < A.ns) S.wsum[warp][base + s] = v;
   }
-  if (TOTAL) {  // slot ns-1 = total - others (per thread, then reduced)
-    const double v = warp_sum_f64(rest);
-    if (lane == 0) S.wsum[warp][A.ns - 1] = v;
-    TL_STAMP(ts) ts[25] = gtimer_after(v);
+  if (TOTAL) vals[C] = rest;
+  if constexpr (V > 0) {
+    int idx = 0;
+    const double v = warp_xreduce<V, 4>(vals, lane, idx);
+    if ((lane & xreduce_group_mask(V)) == 0) {
+      const int slot = idx < C ? base + idx : A.ns - 1;
+      if (idx < V && (idx >= C || base + idx < A.ns)) S.wsum[warp][slot] = v;
+    }
+    TL_STAMP(ts && TOTAL) ts[25] = gtimer_after(v);
   }
 }
 
