@@ -108,6 +108,15 @@ int bart_shard_connect(bart_chain *h, const void *all /* n_shards * BART_SHARD_H
 /* Test hook: emulate `groups` shards inside one launch on one device (CTA c
  * polls copy c % groups; every CTA adds into every copy). */
 int bart_set_copy_groups(bart_chain *h, int groups);
+/* Cross-CTA / cross-shard exchange of the per-tree leaf sums and counts.
+ * FLAT: every CTA of every shard adds into every shard's words (n_shards x CTAs
+ * arrivals per word).  TWO_LEVEL: CTAs add into their own shard's stage words;
+ * one forwarder CTA per shard adds the shard's total into every shard's words
+ * (n_shards arrivals per word, one remote add per shard).  Totals, hence every
+ * decision, are bit-identical between the two.  Set between steps. */
+#define BART_EXCHANGE_FLAT 0
+#define BART_EXCHANGE_TWO_LEVEL 1
+int bart_set_exchange(bart_chain *h, int mode);
 
 /* Direct state edit + SamplerState.rebuild_structure_caches (sampler.py:157-168,
  * tests/util.py:11-24).  axis (m, 2^(D-1)) as uint16; leaf_index (n, m) or NULL

@@ -82,6 +82,7 @@ _SIGS = {
     "bart_get_accepted": [_P, _P],
     "bart_get_proposals": [_P, _P, _P],
     "bart_get_randoms": [_P, _P, _P, _P, _P],
+    "bart_set_exchange": [_P, C.c_int],
     "bart_philox4x32_10": [_P, _P, _P, C.c_int64, C.c_int],
     "bart_set_taps": [_P, C.c_int],
     "bart_get_taps": [_P, _P, _P],

@@ -529,6 +529,10 @@ int bart_shard_connect(bart_chain *h, const void *all) {
   c.shard_sys = 1;
   h->shard_pending = false;
   drop_graphs(h);  // captured launches carry the chain parameters
+  // from 4 shards the flat exchange's arrivals (CTAs x shards per word)
+  // outgrow the two-level exchange's extra hop (tools/xshard_bench.cu:
+  // 3295 vs 3002 cycles at N=4, 4989 vs 3091 at N=8)
+  if (c.n_shards >= 4) return bart_set_exchange(h, BART_EXCHANGE_TWO_LEVEL);
   return BART_OK;
 }
 
@@ -555,6 +559,27 @@ int bart_set_copy_groups(bart_chain *h, int groups) {
   return BART_OK;
 }
 
+
+int bart_set_exchange(bart_chain *h, int mode) {
+  if (!h) return fail(BART_EINVAL, "NULL handle");
+  if (mode != BART_EXCHANGE_FLAT && mode != BART_EXCHANGE_TWO_LEVEL)
+    return fail(BART_EINVAL, "exchange mode must be BART_EXCHANGE_FLAT or BART_EXCHANGE_TWO_LEVEL");
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ChainDev &c = h->c;
+  if (mode == BART_EXCHANGE_TWO_LEVEL && !c.xstage) {
+    // stage words and forwarder baselines for up to kMaxShards copy groups
+    // (one per emulated shard; a real shard uses group 0), zero: a fresh stage
+    CUDA_TRY(own(h, &c.xstage, (size_t)kMaxShards * kXSets * kXSetWords));
+    CUDA_TRY(own(h, &c.cstage, (size_t)kMaxShards * kCSets * kCSetWords));
+    CUDA_TRY(own(h, &c.xssnap, (size_t)kMaxShards * kXSets * kXPrevWords));
+    CUDA_TRY(own(h, &c.cssnap, (size_t)kMaxShards * kCSets * kCSetWords));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  c.hier = mode == BART_EXCHANGE_TWO_LEVEL ? 1 : 0;
+  drop_graphs(h);  // captured launches carry the chain parameters
+  return BART_OK;
+}
 
 int bart_trace_begin(bart_chain *h, const bart_trace_opts *o, const uint8_t *X_test) {
   if (!h || !o) return fail(BART_EINVAL, "NULL argument");

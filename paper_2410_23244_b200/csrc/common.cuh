@@ -117,6 +117,16 @@ struct ChainDev {
   unsigned long long *cacc;     // this shard's count channel [kCSets][kCSetWords] (polled)
   unsigned long long *cpeer[kMaxShards];  // every shard's cacc
   unsigned long long *csnap;    // [kCSets*kCSetWords] last complete count words
+  // Two-level (hierarchical) exchange, n-sharded chains: a CTA adds into its
+  // own shard's STAGE words (device scope); one forwarder CTA per shard polls
+  // them complete and adds the shard's total, tagged once, into every shard's
+  // copy -- n_shards arrivals per word instead of one per CTA of every shard.
+  // With copy groups (one-device emulation) every group has its own stage.
+  int hier;                      // 1: two-level exchange (bart_set_exchange)
+  unsigned long long *xstage;    // [groups][kXSets][kXSetWords] (groups = copy_groups, or 1 per shard)
+  unsigned long long *cstage;    // [groups][kCSets][kCSetWords]
+  unsigned long long *xssnap;    // [groups][kXSets*kXPrevWords] forwarders' stage baselines
+  unsigned long long *cssnap;    // [groups][kCSets*kCSetWords]
   unsigned long long *iter_dev;
   uint64_t seed;
   int nblk, chunk;

@@ -93,6 +93,8 @@ struct __align__(16) SweepSmem {
   float dlt[256];                           // residual delta by larger-tree heap index
   unsigned long long xprev[kXSets][kXPrevWords];      // last complete value of every exchange word (s*4+q)
   unsigned long long cprev[kCSets][kCSetWords];       // last complete value of every count word
+  unsigned long long xsprev[kXSets][kXPrevWords];     // two-level exchange, forwarder: stage baselines
+  unsigned long long csprev[kCSets][kCSetWords];
   unsigned long long mbar[kRing];      // TMA ring slot filled (per tree j % kRing)
   unsigned long long cnt_mbar[2];     // workers -> helper: B pass counts of tree t in wcnt[t & 1]
   unsigned long long prep_mbar[2];    // helper -> control: prep[t & 1] ready
@@ -253,6 +255,31 @@ __device__ __forceinline__ double warp_xreduce(const double (&a)[N], int lane, i
 __host__ __device__ constexpr int xreduce_levels(int n) { return n <= 1 ? 0 : 1 + xreduce_levels((n + 1) / 2); }
 __host__ __device__ constexpr int xreduce_group_mask(int n) { return (1 << (5 - xreduce_levels(n))) - 1; }
 
+// Per-warp slot sums -> S.wsum[warp]: the C compared slots [base, base+C)
+// and (TOTAL) slot ns-1 = per-thread total minus the others, reduced together.
+template <int C, bool TOTAL>
+__device__ __forceinline__ void store_warp_sums(const double (&acc)[C > 0 ? C : 1], double tot, const APass &A,
+                                                SweepSmem &S, int warp, int lane, int base, long long *ts = nullptr) {
+  constexpr int V = C + (TOTAL ? 1 : 0);
+  double vals[V > 0 ? V : 1];
+  double rest = tot;
+#pragma unroll
+  for (int s = 0; s < C; ++s) {
+    vals[s] = acc[s];
+    if (TOTAL) rest = __dsub_rn(rest, acc[s]);
+  }
+  if (TOTAL) vals[C] = rest;
+  if constexpr (V > 0) {
+    int idx = 0;
+    const double v = warp_xreduce<V, 4>(vals, lane, idx);
+    if ((lane & xreduce_group_mask(V)) == 0) {
+      const int slot = idx < C ? base + idx : A.ns - 1;
+      if (idx < V && (idx >= C || base + idx < A.ns)) S.wsum[warp][slot] = v;
+    }
+    TL_STAMP(ts && TOTAL) ts[25] = gtimer_after(v);
+  }
+}
+
 // A pass over the register-resident chunk.  FIRST: tree e-1's update
 // (residuals f32 with the reference's two roundings, sampler.py:755-760;
 // cache write of the final tree).  Then the f64 residual sums of tree e over
@@ -292,25 +319,7 @@ __device__ __forceinline__ void sums_pass(float4 (&r)[W], const uint32_t (&lp)[W
     }
   }
   TL_STAMP(ts && base == 0) ts[24] = gtimer_after(tot + (C > 0 ? acc[0] : 0.0));
-  // the C compared slots, then (TOTAL) slot ns-1 = total - others per thread
-  constexpr int V = C + (TOTAL ? 1 : 0);
-  double vals[V > 0 ? V : 1];
-  double rest = tot;
-#pragma unroll
-  for (int s = 0; s < C; ++s) {
-    vals[s] = acc[s];
-    if (TOTAL) rest = __dsub_rn(rest, acc[s]);
-  }
-  if (TOTAL) vals[C] = rest;
-  if constexpr (V > 0) {
-    int idx = 0;
-    const double v = warp_xreduce<V, 4>(vals, lane, idx);
-    if ((lane & xreduce_group_mask(V)) == 0) {
-      const int slot = idx < C ? base + idx : A.ns - 1;
-      if (idx < V && (idx >= C || base + idx < A.ns)) S.wsum[warp][slot] = v;
-    }
-    TL_STAMP(ts && TOTAL) ts[25] = gtimer_after(v);
-  }
+  store_warp_sums<C, TOTAL>(acc, tot, A, S, warp, lane, base, ts);
 }
 
 template <int W>
@@ -512,17 +521,32 @@ __device__ __forceinline__ double xrange_limit(int ctas) {
   while ((1 << bits) < ctas) ++bits;
   return ldexp(1.0, 46 - bits);
 }
+// the copy group (emulated shard) of a CTA: its index among the groups this
+// launch holds, and how many of the launch's CTAs share it
+__host__ __device__ __forceinline__ int xgroup(const ChainDev &c, int cta) {
+  return c.copy_groups > 1 ? cta % c.copy_groups : 0;
+}
+__host__ __device__ __forceinline__ int xgroup_ctas(const ChainDev &c, int grp) {
+  return c.copy_groups > 1 ? (c.nblk - grp + c.copy_groups - 1) / c.copy_groups : c.nblk;
+}
+
 struct XCtx {
-  unsigned long long *xacc, *cacc;
+  unsigned long long *xacc, *cacc;  // the copy this CTA polls
+  unsigned long long *xstage, *cstage;  // two-level: this CTA's stage words (adds), the forwarder polls them
   int *err;
   int n_shards, nblk_total;
-  bool sys;
+  int target;    // arrivals of a complete copy word: CTAs of all shards, or (two-level) shards
+  int grp_ctas;  // two-level: arrivals of a complete stage word
+  bool sys, hier, fwd;
   double lim;  // per-CTA fixed-point range (to_limbs)
-  // xacc/cacc: the copy this CTA polls
   __device__ __forceinline__ XCtx(const ChainDev &c, int cta)
       : xacc(pin_ptr(c.copy_groups > 1 ? c.xpeer[c.copy_base + cta % c.copy_groups] : c.xacc)),
-        cacc(pin_ptr(c.copy_groups > 1 ? c.cpeer[c.copy_base + cta % c.copy_groups] : c.cacc)), err(pin_ptr(c.err)),
-        n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)), sys(pin_int(c.shard_sys) != 0),
+        cacc(pin_ptr(c.copy_groups > 1 ? c.cpeer[c.copy_base + cta % c.copy_groups] : c.cacc)),
+        xstage(pin_ptr(c.hier ? c.xstage + (size_t)xgroup(c, cta) * kXSets * kXSetWords : nullptr)),
+        cstage(pin_ptr(c.hier ? c.cstage + (size_t)xgroup(c, cta) * kCSets * kCSetWords : nullptr)),
+        err(pin_ptr(c.err)), n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)),
+        target(pin_int(c.hier ? c.n_shards : c.nblk_total)), grp_ctas(pin_int(xgroup_ctas(c, xgroup(c, cta)))),
+        sys(pin_int(c.shard_sys) != 0), hier(c.hier != 0), fwd(c.hier != 0 && cta == xgroup(c, cta)),
         lim(xrange_limit(c.nblk_total)) {}
 };
 
@@ -556,7 +580,9 @@ __device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx &X, c
       TL_STAMP(ts && s0 == 0) ts[15] = gtimer_after(__longlong_as_double((long long)(l[2] | l[1] | l[0])));
       if (q < 3) {
         const unsigned long long v = kTagOne | pick3(l, q);
-        if (X.n_shards == 1)
+        if (X.hier)
+          red_add(X.xstage + set_off + (size_t)s * kXSlotWords + q, v, false);
+        else if (X.n_shards == 1)
           red_add(X.xacc + set_off + (size_t)s * kXSlotWords + q, v, false);
         else
           for (int g = 0; g < X.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, v, sys);
@@ -579,7 +605,7 @@ template <int R>
 __device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns, int set, int k0, int lane,
                                             double (&tot)[R], long long *ts = nullptr) {
   const bool sys = X.sys;
-  const unsigned long long target = (unsigned long long)X.nblk_total << kTagShift;
+  const unsigned long long target = (unsigned long long)X.target << kTagShift;
   const unsigned long long *base = X.xacc + (size_t)set * kXSetWords;
   unsigned long long *prev = S.xprev[set];
   const int q = lane & 3;
@@ -658,16 +684,76 @@ __device__ __forceinline__ void counts_add(const ChainDev &c, const XCtx &X, con
     uint32_t cn = 0;
 #pragma unroll
     for (int k = 0; k < kWorkWarps; ++k) cn += S.wcnt[j & 1][k][s];
-    if (X.n_shards == 1)
+    if (X.hier)
+      red_add(X.cstage + off + s, kTagOne | (unsigned long long)cn, false);
+    else if (X.n_shards == 1)
       red_add(X.cacc + off + s, kTagOne | (unsigned long long)cn, false);
     else
       for (int g = 0; g < X.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | (unsigned long long)cn, sys);
   }
 }
 
+// Two-level exchange, the shard's forwarder CTA (control warp): poll this
+// shard's stage words of set `set` until every CTA of the shard has added,
+// then add the shard's totals -- one tagged arrival per word -- into every
+// shard's copy.  Integer sums, so the final totals equal the flat exchange's.
+__device__ __forceinline__ void forward_stage(const ChainDev &c, const XCtx &X, SweepSmem &S, int ns, int set,
+                                              int lane) {
+  const unsigned long long target = (unsigned long long)X.grp_ctas << kTagShift;
+  const size_t set_off = (size_t)set * kXSetWords;
+  const int q = lane & 3;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    const int s = s0 + (lane >> 2);
+    const bool mine = s < ns && q < 3;
+    unsigned long long w = 0ull;
+    bool done;
+    do {
+      bool ok = true;
+      if (mine) {
+        ld_poll1(X.xstage + set_off + (size_t)s * kXSlotWords + q, w);
+        ok = ((w - S.xsprev[set][s * 4 + q]) & ~kDataMask) == target;
+      }
+      done = __all_sync(0xffffffffu, ok);
+    } while (!done);
+    if (mine) {
+      const unsigned long long d = (w - S.xsprev[set][s * 4 + q]) & kDataMask;
+      S.xsprev[set][s * 4 + q] = w;
+      for (int g = 0; g < X.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, kTagOne | d, X.sys);
+    }
+  }
+  __syncwarp();
+}
+
+// The same for the count channel (helper warp of the forwarder CTA).
+__device__ __forceinline__ void forward_counts(const ChainDev &c, const XCtx &X, SweepSmem &S, int j, int ns,
+                                               int lane) {
+  const unsigned long long target = (unsigned long long)X.grp_ctas << kTagShift;
+  const int set = j % kCSets;
+  const size_t off = (size_t)set * kCSetWords;
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int s = s0 + lane;
+    unsigned long long v = 0ull;
+    bool done;
+    do {
+      bool ok = true;
+      if (s < ns) {
+        ld_poll1(X.cstage + off + s, v);
+        ok = ((v - S.csprev[set][s]) & ~kDataMask) == target;
+      }
+      done = __all_sync(0xffffffffu, ok);
+    } while (!done);
+    if (s < ns) {
+      const unsigned long long d = (v - S.csprev[set][s]) & kDataMask;
+      S.csprev[set][s] = v;
+      for (int g = 0; g < X.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | d, X.sys);
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void counts_poll(const XCtx &X, SweepSmem &S, int j, int ns, int lane) {
   const bool sys = X.sys;
-  const unsigned long long target = (unsigned long long)X.nblk_total << kTagShift;
+  const unsigned long long target = (unsigned long long)X.target << kTagShift;
   const int set = j % kCSets;
   const unsigned long long *base = X.cacc + (size_t)set * kCSetWords;
   for (int s0 = 0; s0 < ns; s0 += 32) {
@@ -1147,17 +1233,7 @@ __device__ __forceinline__ void stream_sums(const ChainDev &c, const Geom &G, co
       }
     }
   }
-  double rest = tot;
-#pragma unroll
-  for (int s = 0; s < C; ++s) {
-    const double v = warp_sum_f64(acc[s]);
-    if (TOTAL) rest = __dsub_rn(rest, acc[s]);
-    if (lane == 0 && base + s < A.ns) S.wsum[warp][base + s] = v;
-  }
-  if (TOTAL) {
-    const double v = warp_sum_f64(rest);
-    if (lane == 0) S.wsum[warp][A.ns - 1] = v;
-  }
+  store_warp_sums<C, TOTAL>(acc, tot, A, S, warp, lane, base);
 }
 
 __device__ __forceinline__ void stream_sums_all(const ChainDev &c, const Geom &G, const APass &A, const uint32_t *lp32,
@@ -1334,6 +1410,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 #endif
     long long *ts = tl ? tl + (size_t)(e + 1) * 32 : nullptr;
     exchange_add(c, X, S, ns, set, lane, ts);
+    if (X.fwd) forward_stage(c, X, S, ns, set, lane);
     TL_STAMP(ts) ts[5] = gtimer();
     DecIn I;
     if (has_cur) {
@@ -1404,12 +1481,14 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
     mbar_wait(&S.cnt_mbar[j & 1], par2(j));
     counts_add(c, X, S, j, G.hdr[j].nslots, lane);
+    if (X.fwd) forward_counts(c, X, S, j, G.hdr[j].nslots, lane);
   }
   if (m > 0) prepare_tree(0);
   for (int e = 0; e <= m; ++e) {
     if (e + 2 < m) {  // B_e done: publish the counts of tree e+2
       mbar_wait(&S.cnt_mbar[e & 1], par2(e + 2));
       counts_add(c, X, S, e + 2, G.hdr[e + 2].nslots, lane);
+      if (X.fwd) forward_counts(c, X, S, e + 2, G.hdr[e + 2].nslots, lane);
     }
     // tree e+1's count-only terms: prep[(e+1)&1] was last read by decide(e-1)
     // and decide_post(e-1), both done
@@ -1425,6 +1504,13 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
       if (hp.update_sigma) *c.sigma2 = s2;
       if (hist_row >= 0) c.sig_hist[hist_row] = hp.update_sigma ? s2 : *c.sigma2;
       *c.iter_dev += 1ull;
+    }
+    if (e == m && X.fwd) {  // two-level: this forwarder's stage baselines, for the next sweep
+      const size_t g = (size_t)xgroup(c, G.cta);
+      const unsigned long long *src = &S.xsprev[0][0];
+      for (int i = lane; i < kXSets * (int)kXPrevWords; i += 32) c.xssnap[g * kXSets * kXPrevWords + i] = src[i];
+      const unsigned long long *cs = &S.csprev[0][0];
+      for (int i = lane; i < kCSets * (int)kCSetWords; i += 32) c.cssnap[g * kCSets * kCSetWords + i] = cs[i];
     }
     if (e == m && G.cta == 0) {  // the next sweep's exchange baselines
       if (lane == 0) c.xsnap[0] = xbase + (unsigned long long)(m + 1);
@@ -1480,6 +1566,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
     for (int i = tid; i < kXSets * (int)kXPrevWords; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
     unsigned long long *cd = &S.cprev[0][0];
     for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cd[i] = c.csnap[i];
+    if (c.hier && G.cta == xgroup(c, G.cta)) {  // two-level forwarder: its stage baselines
+      const size_t g = (size_t)xgroup(c, G.cta);
+      unsigned long long *xs = &S.xsprev[0][0];
+      for (int i = tid; i < kXSets * (int)kXPrevWords; i += kSweepThreads) xs[i] = c.xssnap[g * kXSets * kXPrevWords + i];
+      unsigned long long *cs = &S.csprev[0][0];
+      for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cs[i] = c.cssnap[g * kCSets * kCSetWords + i];
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < kRing; ++q) mbar_init(&S.mbar[q]);

@@ -464,6 +464,15 @@ class SamplerState:
     def trace_end(self) -> None:
         N.check(N.lib().bart_trace_end(self._h))
 
+    def set_exchange(self, mode: str) -> None:
+        """The cross-CTA / cross-shard exchange: "flat" (every CTA adds into
+        every shard's words) or "two_level" (per-shard stage, one forwarder
+        per shard); bit-identical results (include/bart_b200.h)."""
+        modes = {"flat": 0, "two_level": 1}
+        if mode not in modes:
+            raise ValueError(f"exchange mode must be one of {sorted(modes)}")
+        N.check(N.lib().bart_set_exchange(self._h, modes[mode]))
+
     def set_copy_groups(self, groups: int) -> None:
         """Test hook: emulate `groups` shards inside one launch on one device."""
         N.check(N.lib().bart_set_copy_groups(self._h, int(groups)))

@@ -250,8 +250,9 @@ def test_stream_mode_large_n_invariants():
     st.close()
 
 
+@pytest.mark.parametrize("mode", ["flat", "two_level"])
 @pytest.mark.parametrize("groups", [2, 3, 8])
-def test_sharded_exchange_emulated(groups):
+def test_sharded_exchange_emulated(groups, mode):
     """n-sharding's exchange protocol (every shard adds into every shard's
     words, each polls its own copy), emulated by splitting one
     launch's CTAs into `groups` copy groups: decisions, counts and indices stay
@@ -267,6 +268,7 @@ def test_sharded_exchange_emulated(groups):
     y32 = ys.forward(y).astype(np.float32)
     st = init_state(Xq, g.counts, y32, hp, None)
     st.set_copy_groups(groups)
+    st.set_exchange(mode)
     st.enable_taps(True)
     ora = OracleChain(Xq, g.counts, y32, hp)
     rng = np.random.default_rng(groups)
@@ -329,3 +331,30 @@ def test_pipelined_step_results_match_synchronous_reads():
         b.step_result(0)  # only the last two steps are kept
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("groups", [1, 2, 8])
+def test_two_level_exchange_bit_identical_to_flat(groups, sweep_mode):
+    """The two-level exchange (per-shard stage words + one forwarder per shard)
+    sums the same integers as the flat one: a device-RNG chain takes the same
+    decisions and ends in the same state, bit for bit, in both modes."""
+    from paper_2410_23244_b200.dgp import friedman1_binned
+    from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
+    from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
+    Xq, y, _, grid = friedman1_binned(60_013, 12, seed=5)
+    hp, ys = derive_hyperparams(y, FitConfig(n_trees=40))
+    y32 = ys.forward(y).astype(np.float32)
+    out = []
+    for mode in ("flat", "two_level"):
+        st = init_state(Xq, grid.counts, y32, hp, DeviceRNG(77))
+        if groups > 1:
+            st.set_copy_groups(groups)
+        st.set_exchange(mode)
+        run(st, hp, 3)
+        st.set_exchange("flat" if mode == "two_level" else "two_level")  # switching between launches
+        run(st, hp, 3)
+        f = st.forest
+        out.append((f.axis.copy(), f.cutpoint.copy(), f.leaf_value.copy(), st.resid.copy(), st.sigma2))
+        st.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)

@@ -26,7 +26,7 @@ from oracle.bart_oracle import OracleChain
 pytestmark = pytest.mark.gpu
 
 
-def _burned_pair(n, p, m, burn, seed, groups=1):
+def _burned_pair(n, p, m, burn, seed, groups=1, exchange="flat"):
     from paper_2410_23244_b200.dgp import friedman1_binned
     from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
     from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
@@ -36,6 +36,7 @@ def _burned_pair(n, p, m, burn, seed, groups=1):
     st = init_state(Xq, grid.counts, y32, hp, DeviceRNG(seed + 100))
     if groups > 1:
         st.set_copy_groups(groups)
+    st.set_exchange(exchange)
     run(st, hp, burn)
     f = st.forest
     ora = OracleChain(Xq, grid.counts, y32, hp, sigma2=st.sigma2, axis=f.axis, cut=f.cutpoint, leaf=f.leaf_value,
@@ -99,12 +100,14 @@ def test_benchmark_shape_matches_oracle(shape):
     st.close()
 
 
-def test_eight_copy_groups_at_shard_shape():
+@pytest.mark.parametrize("exchange", ["flat", "two_level"])
+def test_eight_copy_groups_at_shard_shape(exchange):
     """One GPU standing in for an 8-way n-sharded chain of configs[3] (n=1e7
     over 8 GPUs = 1.25e6 points per shard): 148 CTAs in 8 copy groups, each
-    polling its own exchange copy while every CTA adds into all 8 copies
-     -- the W=8 instantiation with the sharded exchange."""
-    st, ora, hp, n = _burned_pair(1_250_000, 100, 200, 30, seed=3, groups=8)
+    polling its own exchange copy -- every CTA adding into all 8 copies (flat),
+    or each group's forwarder adding its group's total (two_level; DESIGN.md
+    §6) -- the W=8 instantiation with the sharded exchange."""
+    st, ora, hp, n = _burned_pair(1_250_000, 100, 200, 30, seed=3, groups=8, exchange=exchange)
     cfg = st.sweep_config()
     assert cfg["ctas"] == 148 and _words(cfg["chunk"]) == 8
     _compare_steps(st, ora, hp, n, 3, seed=8)

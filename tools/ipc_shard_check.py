@@ -2,7 +2,7 @@
 
 Run with torchrun (gloo for the one-time handle all-gather):
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
-        --master-port 29561 tools/ipc_shard_check.py [n] [trees] [iters]
+        --master-port 29561 tools/ipc_shard_check.py [n] [trees] [iters] [flat|two_level]
 
 Every rank uses device LOCAL_RANK % device_count, so on a one-GPU box both
 shards share the GPU: their sweeps then progress by time-slicing (one context
@@ -33,6 +33,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 3000
     m = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    mode = sys.argv[4] if len(sys.argv) > 4 else "flat"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     device = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
@@ -46,6 +47,8 @@ def main():
     lo, hi = plan.bounds(rank)
     st = init_sharded_state(Xq[lo:hi], g.counts, y32[lo:hi], hp, DeviceRNG(42), plan, rank, s2, torch_all_gather(),
                             device=device)
+    st.set_exchange(mode)
+    cfg = st.sweep_config()
     run(st, hp, iters)
     st.sync()
     f = st.forest
@@ -69,7 +72,8 @@ def main():
         resid_ok = np.allclose(ref.resid, full_r, rtol=1e-5, atol=1e-5)
         ref.close()
         ok = same and cut_ok and leaf_ok and resid_ok
-        print(f"ipc shard check: world={world} n={n} trees={m} iters={iters}: shards identical={same} "
+        print(f"ipc shard check: world={world} n={n} trees={m} iters={iters} exchange={mode} "
+              f"ctas/shard={cfg['ctas']} chunk={cfg['chunk']}: shards identical={same} "
               f"structure==unsharded={cut_ok} leaves~={leaf_ok} resid~={resid_ok} -> {'OK' if ok else 'FAIL'}",
               flush=True)
     dist.barrier()
