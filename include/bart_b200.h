@@ -195,6 +195,11 @@ int bart_get_trace(bart_chain *h, int64_t *out);
 typedef struct {
   int64_t n_iter, n_keep, n_test;  /* capacities; n_test rows of X_test */
   int32_t store_train_draws, store_forests;
+  /* training-row draws kept on the device: 0 = all n_keep; else a ring of
+   * train_ring rows (kept draw k in row k % train_ring), drained by the
+   * caller with bart_trace_read_draws before it is overwritten -- a streamed
+   * trace file then needs train_ring * n * 8 B of device memory, not n_keep * n * 8 */
+  int64_t train_ring;
 } bart_trace_opts;
 int bart_trace_begin(bart_chain *h, const bart_trace_opts *opts, const uint8_t *X_test /* (n_test, p) or NULL */);
 int bart_trace_keep(bart_chain *h);
@@ -206,7 +211,8 @@ int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, doubl
                     double *train_var, double *train_draws, double *train_points, double *test_draws,
                     double *mean_leaves, uint16_t *axis, uint8_t *cutpoint, float *leaf_value);
 /* kept draws [k0, k1) only: train (k1-k0, n) / test (k1-k0, n_test), either NULL
- * (streams a BFTRACE1 file from the device without one host array of every draw) */
+ * (streams a BFTRACE1 file from the device without one host array of every draw);
+ * with a train ring, [k0, k1) must still be in it (k0 >= kept - train_ring) */
 int bart_trace_read_draws(bart_chain *h, int64_t k0, int64_t k1, double *train, double *test);
 int bart_trace_end(bart_chain *h);
 

@@ -35,7 +35,7 @@ class HParams(C.Structure):
 
 class TraceOpts(C.Structure):
     _fields_ = [("n_iter", C.c_int64), ("n_keep", C.c_int64), ("n_test", C.c_int64),
-                ("store_train_draws", C.c_int32), ("store_forests", C.c_int32)]
+                ("store_train_draws", C.c_int32), ("store_forests", C.c_int32), ("train_ring", C.c_int64)]
 
 
 TRACE_POINTS = 8

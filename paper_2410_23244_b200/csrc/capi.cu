@@ -82,6 +82,7 @@ HP to_hp(const bart_hparams *h) {
 struct TraceState {  // fit() trace kept on the device (bart_trace_begin)
   bool on = false;
   int64_t iter_cap = 0, keep_cap = 0, n_test = 0, ld_test = 0, iter0 = 0, kept = 0;
+  int64_t train_rows = 0;  // device rows of training-row draws: keep_cap, or the ring size
   int store_train = 0, store_forests = 0, npts = 0;
   uint8_t *acc = nullptr, *Xt_test = nullptr, *f_cut = nullptr;
   uint16_t *f_axis = nullptr;
@@ -583,7 +584,7 @@ int bart_set_exchange(bart_chain *h, int mode) {
 
 int bart_trace_begin(bart_chain *h, const bart_trace_opts *o, const uint8_t *X_test) {
   if (!h || !o) return fail(BART_EINVAL, "NULL argument");
-  if (o->n_iter < 0 || o->n_keep < 0 || o->n_test < 0 || (o->n_test > 0 && !X_test))
+  if (o->n_iter < 0 || o->n_keep < 0 || o->n_test < 0 || o->train_ring < 0 || (o->n_test > 0 && !X_test))
     return fail(BART_EINVAL, "bad trace options");
   CUDA_TRY(cudaSetDevice(h->device));
   trace_free(h);
@@ -605,7 +606,8 @@ int bart_trace_begin(bart_chain *h, const bart_trace_opts *o, const uint8_t *X_t
   CUDA_TRY(trace_alloc(h, &t.m2, n));
   CUDA_TRY(trace_alloc(h, &t.pts, K * t.npts));
   CUDA_TRY(trace_alloc(h, &t.mleaves, K));
-  if (t.store_train) CUDA_TRY(trace_alloc(h, &t.train, K * n));
+  t.train_rows = (o->train_ring > 0 && o->train_ring < t.keep_cap) ? o->train_ring : t.keep_cap;
+  if (t.store_train) CUDA_TRY(trace_alloc(h, &t.train, (size_t)t.train_rows * n));
   if (t.n_test) {
     CUDA_TRY(trace_alloc(h, &t.test, K * (size_t)t.n_test));
     CUDA_TRY(trace_alloc(h, &t.Xt_test, (size_t)t.ld_test * c.p));
@@ -640,7 +642,7 @@ int bart_trace_keep(bart_chain *h) {
   cudaStream_t s = h->stream;
   const size_t k = (size_t)t.kept;
   launch_trace_train(c.L, c.n, c.n_pad, c.m, c.size, c.leaf, t.kept + 1, t.mean, t.m2,
-                     t.store_train ? t.train + k * c.n : nullptr, t.pts + k * t.npts, t.npts, s);
+                     t.store_train ? t.train + (k % (size_t)t.train_rows) * c.n : nullptr, t.pts + k * t.npts, t.npts, s);
   if (t.n_test)
     launch_evaluate(t.Xt_test, t.n_test, t.ld_test, c.D, c.half, c.m, c.axis, c.cut, c.leaf, t.test + k * t.n_test, s);
   launch_mean_leaves(c.cut, c.m, c.half, t.mleaves + k, s);
@@ -685,7 +687,10 @@ int bart_trace_read(bart_chain *h, uint8_t *accepted, double *sigma2_iter, doubl
     CUDA_TRY(d2h(train_var, t.m2, (size_t)c.n * 8));
     for (int64_t i = 0; i < c.n; ++i) train_var[i] = nk > 1 ? train_var[i] / (double)(nk - 1) : 0.0;
   }
-  if (t.store_train) CUDA_TRY(d2h(train_draws, t.train, (size_t)nk * c.n * 8));
+  if (t.store_train && train_draws) {
+    if (t.train_rows < t.keep_cap) return fail(BART_ESTATE, "training-row draws are in a ring: read them with bart_trace_read_draws");
+    CUDA_TRY(d2h(train_draws, t.train, (size_t)nk * c.n * 8));
+  }
   CUDA_TRY(d2h(train_points, t.pts, (size_t)nk * t.npts * 8));
   if (t.n_test) CUDA_TRY(d2h(test_draws, t.test, (size_t)nk * t.n_test * 8));
   CUDA_TRY(d2h(mean_leaves, t.mleaves, (size_t)nk * 8));
@@ -706,8 +711,15 @@ int bart_trace_read_draws(bart_chain *h, int64_t k0, int64_t k1, double *train, 
   if (test && !t.n_test) return fail(BART_ESTATE, "no test rows in this trace");
   if (int rc = bart_sync(h)) return rc;
   const size_t rows = (size_t)(k1 - k0);
-  if (train && rows)
-    CUDA_TRY(cudaMemcpy(train, t.train + (size_t)k0 * h->c.n, rows * h->c.n * 8, cudaMemcpyDeviceToHost));
+  if (train && rows) {
+    if (k0 < nk - t.train_rows) return fail(BART_EINVAL, "draw range no longer in the device ring (train_ring)");
+    const size_t n = (size_t)h->c.n;
+    for (size_t k = (size_t)k0; k < (size_t)k1;) {  // contiguous runs of ring rows
+      const size_t r = k % (size_t)t.train_rows, run = std::min((size_t)k1 - k, (size_t)t.train_rows - r);
+      CUDA_TRY(cudaMemcpy(train + (k - (size_t)k0) * n, t.train + r * n, run * n * 8, cudaMemcpyDeviceToHost));
+      k += run;
+    }
+  }
   if (test && rows)
     CUDA_TRY(cudaMemcpy(test, t.test + (size_t)k0 * t.n_test, rows * t.n_test * 8, cudaMemcpyDeviceToHost));
   return BART_OK;

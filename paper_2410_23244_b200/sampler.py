@@ -4,8 +4,9 @@
 (sampler.py:201-241, 878-912): the chain state lives on the device behind an
 opaque C handle (include/bart_b200.h) and `SamplerState` exposes it through
 the reference's attribute names, fetched lazily in the reference's layouts.
-One `step` = two kernel launches: the tree-parallel proposal kernel and the
-persistent sweep kernel that runs phases 2-11 and the sigma draw.
+One `step` = ONE kernel launch: the persistent sweep kernel proposes every
+tree (phase 1, spread over all warps of the grid), then runs phases 2-11 tree
+by tree and the sigma draw (csrc/sweep.cu).
 
 Randomness.  With a numpy `Generator` (the reference's `rng`), `step` draws
 the reference's `StepRandoms` block on the host in the reference's order and
@@ -419,10 +420,12 @@ class SamplerState:
 
     # -- fit() trace kept on the device (bart_trace_*)
     def trace_begin(self, n_iter: int, n_keep: int, Xq_test: np.ndarray | None = None,
-                    store_train_draws: bool = False, store_forests: bool = False) -> None:
+                    store_train_draws: bool = False, store_forests: bool = False, train_ring: int = 0) -> None:
+        """train_ring > 0: keep only that many training-row draws on the device
+        (a ring; drain it with trace_read_draws before it wraps)."""
         X = None if Xq_test is None else np.ascontiguousarray(Xq_test, np.uint8)
         opts = N.TraceOpts(int(n_iter), int(n_keep), 0 if X is None else int(X.shape[0]),
-                           int(bool(store_train_draws)), int(bool(store_forests)))
+                           int(bool(store_train_draws)), int(bool(store_forests)), int(train_ring))
         N.check(N.lib().bart_trace_begin(self._h, C.byref(opts), N.ptr(X)))
         self._trace = dict(n_test=opts.n_test, store_train=bool(store_train_draws), store_forests=bool(store_forests))
 

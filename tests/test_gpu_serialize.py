@@ -42,6 +42,52 @@ def test_fit_streams_trace_file(tmp_path, with_test):
     np.testing.assert_array_equal(whole.yhat_train, got.yhat_train)
 
 
+def test_fit_streams_trace_through_device_ring(tmp_path, monkeypatch):
+    """With a 4-draw device ring (the ring a huge n * n_kept would get), the
+    streamed file still holds every kept draw: the ring is drained to the file
+    as it fills (bounded device memory for streamed traces)."""
+    from paper_2410_23244_b200 import regression, serialize
+    from paper_2410_23244_b200.regression import FitConfig, fit
+    X, y = _data()
+    base = dict(n_trees=20, n_burn=10, n_kept=11, thinning=1, n_chains=2, seed=6)
+    full = fit(X, y, FitConfig(**base, keep_train_draws=True))
+    monkeypatch.setattr(regression, "_TRACE_RING_BYTES", 4 * 8 * X.shape[0])  # -> 4 rows per chain
+    path = tmp_path / "ring.bftrace"
+    fit(X, y, FitConfig(**base, keep_train_draws=False), trace_path=str(path))
+    got = serialize.load_trace(str(path))
+    np.testing.assert_array_equal(got.yhat_train, full.yhat_train)
+
+
+def test_trace_ring_windows():
+    """bart_trace_read_draws over a ring: windows still in it read back exactly
+    (also across the wrap), older ones are refused, the whole-trace read too."""
+    from paper_2410_23244_b200.sampler import DeviceRNG, Hyperparams, init_state, run
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 10, (500, 3)).astype(np.uint8)
+    hp = Hyperparams(leaf_sd=0.3, lam=0.1, n_trees=5, max_depth=4)
+    y = rng.normal(size=500).astype(np.float32)
+    a = init_state(X, np.full(3, 9), y, hp, DeviceRNG(8), sigma2=1.0)
+    b = init_state(X, np.full(3, 9), y, hp, DeviceRNG(8), sigma2=1.0)
+    a.trace_begin(20, 10, store_train_draws=True)
+    b.trace_begin(20, 10, store_train_draws=True, train_ring=3)
+    got = []
+    for k in range(10):
+        for st in (a, b):
+            run(st, hp, 2)
+            st.trace_keep()
+        if k % 3 == 2:  # drain b's ring every 3 draws
+            got.append(b.trace_read_draws(k - 2, k + 1)[0])
+    want = a.trace_read_draws(0, 10)[0]
+    np.testing.assert_array_equal(np.concatenate(got), want[:9])
+    np.testing.assert_array_equal(b.trace_read_draws(8, 10)[0], want[8:10])  # wraps the ring end
+    with pytest.raises(ValueError):
+        b.trace_read_draws(5, 8)  # overwritten
+    with pytest.raises(RuntimeError):
+        b.trace_read(train_draws=True)
+    a.close()
+    b.close()
+
+
 @pytest.mark.parametrize("rng_kind", ["device", "numpy"])
 def test_checkpoint_resume_is_bit_identical(tmp_path, rng_kind):
     from paper_2410_23244_b200 import serialize
