@@ -122,7 +122,10 @@ def load_library(path: str | None = None) -> C.CDLL:
             f"CUDA library {path} is missing; build it with `python -m paper_2410_23244_b200._build` "
             "(there is no CPU fallback)")
     lib = C.CDLL(path)
+    variant = path != LIB  # an A/B build of an older revision may lack newer entry points
     for name, args in _SIGS.items():
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int

@@ -309,7 +309,7 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
     if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) c.persist_bytes = want;
     cudaGetLastError();
   }
-  h->smem = sweep_smem_bytes(c.m, c.chunk, c.size, c.stream != 0);
+  h->smem = sweep_smem_bytes(c.m, c.chunk, c.size, c.stream != 0, false);
   if ((int64_t)h->smem > optin)
     return bail(fail(BART_EINVAL, "sweep needs " + std::to_string(h->smem) + " B shared memory > " +
                                       std::to_string(optin) + " (n_trees too large?)"));
@@ -577,6 +577,15 @@ int bart_set_exchange(bart_chain *h, int mode) {
     CUDA_TRY(own(h, &c.cssnap, (size_t)kMaxShards * kCSets * kCSetWords));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
+  // the two-level kernel keeps its forwarder baselines after the TMA ring
+  const size_t smem = sweep_smem_bytes(c.m, c.chunk, c.size, c.stream != 0, mode == BART_EXCHANGE_TWO_LEVEL);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+  if ((int64_t)smem > optin) return fail(BART_EINVAL, "two-level exchange needs " + std::to_string(smem) +
+                                                         " B of shared memory > " + std::to_string(optin));
+  if (cudaError_t e = sweep_prepare(smem); e != cudaSuccess)
+    return fail(BART_ECUDA, std::string("sweep_prepare: ") + cudaGetErrorString(e));
+  h->smem = smem;
   c.hier = mode == BART_EXCHANGE_TWO_LEVEL ? 1 : 0;
   drop_graphs(h);  // captured launches carry the chain parameters
   return BART_OK;

@@ -12,7 +12,7 @@ namespace bart {
 void launch_propose(const ChainDev &c, int device_rng, cudaStream_t s);
 // the step's Philox4x32-10 (common.cuh) on explicit counters/keys: known-answer tests
 void launch_philox(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t count, cudaStream_t s);
-size_t sweep_smem_bytes(int m, int chunk, int size, bool stream);
+size_t sweep_smem_bytes(int m, int chunk, int size, bool stream, bool hier);
 cudaError_t sweep_prepare(size_t smem);
 int sweep_max_ctas(size_t smem, int device, int chunk, bool stream);
 int sweep_words_per_thread(int chunk);

@@ -93,13 +93,18 @@ struct __align__(16) SweepSmem {
   float dlt[256];                           // residual delta by larger-tree heap index
   unsigned long long xprev[kXSets][kXPrevWords];      // last complete value of every exchange word (s*4+q)
   unsigned long long cprev[kCSets][kCSetWords];       // last complete value of every count word
-  unsigned long long xsprev[kXSets][kXPrevWords];     // two-level exchange, forwarder: stage baselines
-  unsigned long long csprev[kCSets][kCSetWords];
   unsigned long long mbar[kRing];      // TMA ring slot filled (per tree j % kRing)
   unsigned long long cnt_mbar[2];     // workers -> helper: B pass counts of tree t in wcnt[t & 1]
   unsigned long long prep_mbar[2];    // helper -> control: prep[t & 1] ready
   unsigned long long dec_mbar[2];     // control -> helper: decision t in dec[t & 1] (t = m: sum r^2)
   int flag_wr, flag_prune, flag_t;
+};
+
+// two-level exchange only (the HIER kernel; after the ring): a forwarder's
+// baselines of its shard's stage words
+struct __align__(16) HierSmem {
+  unsigned long long xsprev[kXSets][kXPrevWords];
+  unsigned long long csprev[kCSets][kCSetWords];
 };
 
 // ring slot: cache row | split column | record (register mode); record only (stream mode)
@@ -117,10 +122,11 @@ int sweep_words_per_thread(int chunk) {
   return 0;
 }
 
-size_t sweep_smem_bytes(int m, int chunk, int size, bool stream) {
+size_t sweep_smem_bytes(int m, int chunk, int size, bool stream, bool hier) {
   size_t b = sizeof(SweepSmem);
   b += ((size_t)m * sizeof(TreeHdr) + 15) & ~(size_t)15;
-  b += (size_t)kRing * ring_slot_bytes(chunk, rec_stride(size), stream);
+  b += ((size_t)kRing * ring_slot_bytes(chunk, rec_stride(size), stream) + 15) & ~(size_t)15;
+  if (hier) b += sizeof(HierSmem);
   return b;
 }
 
@@ -209,6 +215,7 @@ struct Geom {
   uint32_t row_bytes;   // 2 * chunk (register mode) or 0 (stream mode)
   uint8_t *ring;
   TreeHdr *hdr;
+  HierSmem *hs;  // two-level exchange kernel only
   __device__ __forceinline__ uint8_t *slot(int j) const { return ring + (size_t)(j % kRing) * slot_bytes; }
   __device__ __forceinline__ const uint8_t *rec(int j) const { return slot(j) + row_bytes; }
 };
@@ -530,6 +537,9 @@ __host__ __device__ __forceinline__ int xgroup_ctas(const ChainDev &c, int grp) 
   return c.copy_groups > 1 ? (c.nblk - grp + c.copy_groups - 1) / c.copy_groups : c.nblk;
 }
 
+// HIER: the two-level exchange's kernel instantiation; the flat one folds the
+// stage fields away (the flat path's code is what it was before two-level)
+template <bool HIER>
 struct XCtx {
   unsigned long long *xacc, *cacc;  // the copy this CTA polls
   unsigned long long *xstage, *cstage;  // two-level: this CTA's stage words (adds), the forwarder polls them
@@ -542,11 +552,11 @@ struct XCtx {
   __device__ __forceinline__ XCtx(const ChainDev &c, int cta)
       : xacc(pin_ptr(c.copy_groups > 1 ? c.xpeer[c.copy_base + cta % c.copy_groups] : c.xacc)),
         cacc(pin_ptr(c.copy_groups > 1 ? c.cpeer[c.copy_base + cta % c.copy_groups] : c.cacc)),
-        xstage(pin_ptr(c.hier ? c.xstage + (size_t)xgroup(c, cta) * kXSets * kXSetWords : nullptr)),
-        cstage(pin_ptr(c.hier ? c.cstage + (size_t)xgroup(c, cta) * kCSets * kCSetWords : nullptr)),
+        xstage(HIER ? pin_ptr(c.xstage + (size_t)xgroup(c, cta) * kXSets * kXSetWords) : nullptr),
+        cstage(HIER ? pin_ptr(c.cstage + (size_t)xgroup(c, cta) * kCSets * kCSetWords) : nullptr),
         err(pin_ptr(c.err)), n_shards(pin_int(c.n_shards)), nblk_total(pin_int(c.nblk_total)),
-        target(pin_int(c.hier ? c.n_shards : c.nblk_total)), grp_ctas(pin_int(xgroup_ctas(c, xgroup(c, cta)))),
-        sys(pin_int(c.shard_sys) != 0), hier(c.hier != 0), fwd(c.hier != 0 && cta == xgroup(c, cta)),
+        target(HIER ? n_shards : nblk_total), grp_ctas(HIER ? pin_int(xgroup_ctas(c, xgroup(c, cta))) : 0),
+        sys(pin_int(c.shard_sys) != 0), hier(HIER), fwd(HIER && cta == xgroup(c, cta)),
         lim(xrange_limit(c.nblk_total)) {}
 };
 
@@ -559,7 +569,8 @@ __device__ __forceinline__ unsigned long long pick3(const unsigned long long (&l
   return q == 0 ? l[0] : (q == 1 ? l[1] : l[2]);
 }
 
-__device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx &X, const SweepSmem &S, int ns, int set,
+template <bool HIER>
+__device__ __forceinline__ void exchange_add(const ChainDev &c, const XCtx<HIER> &X, const SweepSmem &S, int ns, int set,
                                              int lane, long long *ts = nullptr) {
   const bool sys = X.sys;
   const size_t set_off = (size_t)set * kXSetWords;
@@ -601,8 +612,8 @@ __device__ __forceinline__ void ld_poll1s(const unsigned long long *p, unsigned 
 
 // Poll rounds [k0, k0+R) of set `set` until every used word is complete; on
 // return lane 4j (q == 0) holds in tot[k] the total of slot 8(k0+k)+j.
-template <int R>
-__device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns, int set, int k0, int lane,
+template <int R, bool HIER>
+__device__ __forceinline__ void poll_rounds(const XCtx<HIER> &X, SweepSmem &S, int ns, int set, int k0, int lane,
                                             double (&tot)[R], long long *ts = nullptr) {
   const bool sys = X.sys;
   const unsigned long long target = (unsigned long long)X.target << kTagShift;
@@ -643,17 +654,18 @@ __device__ __forceinline__ void poll_rounds(const XCtx &X, SweepSmem &S, int ns,
 }
 
 // Trees with <= 32 slots: returns the total of slot `lane` in every lane.
-__device__ __forceinline__ double exchange_poll_fast(const XCtx &X, SweepSmem &S, int ns, int set, int lane,
+template <bool HIER>
+__device__ __forceinline__ double exchange_poll_fast(const XCtx<HIER> &X, SweepSmem &S, int ns, int set, int lane,
                                                      long long *ts) {
   const int rounds = (ns + 7) >> 3;
   double mine = 0.0;
   if (rounds <= 1) {
     double t[1];
-    poll_rounds<1>(X, S, ns, set, 0, lane, t, ts);
+    poll_rounds<1, HIER>(X, S, ns, set, 0, lane, t, ts);
     mine = __shfl_sync(0xffffffffu, t[0], (lane & 7) * 4);
   } else {
     double t[kFastRounds];
-    poll_rounds<kFastRounds>(X, S, ns, set, 0, lane, t, ts);
+    poll_rounds<kFastRounds, HIER>(X, S, ns, set, 0, lane, t, ts);
 #pragma unroll
     for (int k = 0; k < kFastRounds; ++k) {
       const double v = __shfl_sync(0xffffffffu, t[k], (lane & 7) * 4);
@@ -664,10 +676,11 @@ __device__ __forceinline__ double exchange_poll_fast(const XCtx &X, SweepSmem &S
 }
 
 // Any number of slots, one round (8 slots) at a time: totals into S.tot_sum.
-__device__ __forceinline__ void exchange_poll_slow(const XCtx &X, SweepSmem &S, int ns, int set, int lane) {
+template <bool HIER>
+__device__ __forceinline__ void exchange_poll_slow(const XCtx<HIER> &X, SweepSmem &S, int ns, int set, int lane) {
   for (int k0 = 0; 8 * k0 < ns; ++k0) {
     double t[1];
-    poll_rounds<1>(X, S, ns, set, k0, lane, t);
+    poll_rounds<1, HIER>(X, S, ns, set, k0, lane, t);
     const int s = 8 * k0 + (lane >> 2);
     if ((lane & 3) == 0 && s < ns) S.tot_sum[s] = t[0];
   }
@@ -676,7 +689,8 @@ __device__ __forceinline__ void exchange_poll_slow(const XCtx &X, SweepSmem &S, 
 
 // Helper warp, count channel: add this CTA's per-leaf counts of tree j into
 // every shard's copy of count set j % 4 / poll the local copy until complete.
-__device__ __forceinline__ void counts_add(const ChainDev &c, const XCtx &X, const SweepSmem &S, int j, int ns,
+template <bool HIER>
+__device__ __forceinline__ void counts_add(const ChainDev &c, const XCtx<HIER> &X, const SweepSmem &S, int j, int ns,
                                            int lane) {
   const bool sys = X.sys;
   const size_t off = (size_t)(j % kCSets) * kCSetWords;
@@ -697,7 +711,8 @@ __device__ __forceinline__ void counts_add(const ChainDev &c, const XCtx &X, con
 // shard's stage words of set `set` until every CTA of the shard has added,
 // then add the shard's totals -- one tagged arrival per word -- into every
 // shard's copy.  Integer sums, so the final totals equal the flat exchange's.
-__device__ __forceinline__ void forward_stage(const ChainDev &c, const XCtx &X, SweepSmem &S, int ns, int set,
+template <bool HIER>
+__device__ __forceinline__ void forward_stage(const ChainDev &c, const XCtx<HIER> &X, const Geom &G, int ns, int set,
                                               int lane) {
   const unsigned long long target = (unsigned long long)X.grp_ctas << kTagShift;
   const size_t set_off = (size_t)set * kXSetWords;
@@ -711,13 +726,13 @@ __device__ __forceinline__ void forward_stage(const ChainDev &c, const XCtx &X, 
       bool ok = true;
       if (mine) {
         ld_poll1(X.xstage + set_off + (size_t)s * kXSlotWords + q, w);
-        ok = ((w - S.xsprev[set][s * 4 + q]) & ~kDataMask) == target;
+        ok = ((w - G.hs->xsprev[set][s * 4 + q]) & ~kDataMask) == target;
       }
       done = __all_sync(0xffffffffu, ok);
     } while (!done);
     if (mine) {
-      const unsigned long long d = (w - S.xsprev[set][s * 4 + q]) & kDataMask;
-      S.xsprev[set][s * 4 + q] = w;
+      const unsigned long long d = (w - G.hs->xsprev[set][s * 4 + q]) & kDataMask;
+      G.hs->xsprev[set][s * 4 + q] = w;
       for (int g = 0; g < X.n_shards; ++g) red_add(c.xpeer[g] + set_off + (size_t)s * kXSlotWords + q, kTagOne | d, X.sys);
     }
   }
@@ -725,7 +740,8 @@ __device__ __forceinline__ void forward_stage(const ChainDev &c, const XCtx &X, 
 }
 
 // The same for the count channel (helper warp of the forwarder CTA).
-__device__ __forceinline__ void forward_counts(const ChainDev &c, const XCtx &X, SweepSmem &S, int j, int ns,
+template <bool HIER>
+__device__ __forceinline__ void forward_counts(const ChainDev &c, const XCtx<HIER> &X, const Geom &G, int j, int ns,
                                                int lane) {
   const unsigned long long target = (unsigned long long)X.grp_ctas << kTagShift;
   const int set = j % kCSets;
@@ -738,20 +754,21 @@ __device__ __forceinline__ void forward_counts(const ChainDev &c, const XCtx &X,
       bool ok = true;
       if (s < ns) {
         ld_poll1(X.cstage + off + s, v);
-        ok = ((v - S.csprev[set][s]) & ~kDataMask) == target;
+        ok = ((v - G.hs->csprev[set][s]) & ~kDataMask) == target;
       }
       done = __all_sync(0xffffffffu, ok);
     } while (!done);
     if (s < ns) {
-      const unsigned long long d = (v - S.csprev[set][s]) & kDataMask;
-      S.csprev[set][s] = v;
+      const unsigned long long d = (v - G.hs->csprev[set][s]) & kDataMask;
+      G.hs->csprev[set][s] = v;
       for (int g = 0; g < X.n_shards; ++g) red_add(c.cpeer[g] + off + s, kTagOne | d, X.sys);
     }
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ void counts_poll(const XCtx &X, SweepSmem &S, int j, int ns, int lane) {
+template <bool HIER>
+__device__ __forceinline__ void counts_poll(const XCtx<HIER> &X, SweepSmem &S, int j, int ns, int lane) {
   const bool sys = X.sys;
   const unsigned long long target = (unsigned long long)X.target << kTagShift;
   const int set = j % kCSets;
@@ -1386,10 +1403,11 @@ __device__ __forceinline__ void stream_worker_loop(const ChainDev &c, SweepSmem 
 }
 
 // Control warp: exchange and decision, nothing else.
+template <bool HIER>
 __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                              const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
-  const XCtx X(c, G.cta);
+  const XCtx<HIER> X(c, G.cta);
   named_sync(BAR_ROLES, kSweepThreads);  // role prologue barrier
   for (int e = 0; e <= m; ++e) {
     const bool has_cur = e < m;
@@ -1410,7 +1428,7 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 #endif
     long long *ts = tl ? tl + (size_t)(e + 1) * 32 : nullptr;
     exchange_add(c, X, S, ns, set, lane, ts);
-    if (X.fwd) forward_stage(c, X, S, ns, set, lane);
+    if (X.fwd) forward_stage(c, X, G, ns, set, lane);
     TL_STAMP(ts) ts[5] = gtimer();
     DecIn I;
     if (has_cur) {
@@ -1445,10 +1463,11 @@ __device__ __forceinline__ void control_loop(const ChainDev &c, SweepSmem &S, co
 }
 
 // Helper warp: prefetch, count channel, count-only precomputation, bookkeeping.
+template <bool HIER>
 __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int lane,
                                             const DecConst &K, unsigned long long xbase, long long *tl) {
   const int m = G.m;
-  const XCtx X(c, G.cta);
+  const XCtx<HIER> X(c, G.cta);
   // trace row of this iteration (read before the sigma CTA bumps the counter)
   const int64_t hrow = c.acc_hist ? (int64_t)*c.iter_dev - c.hist_base : -1;
   const int64_t hist_row = (hrow >= 0 && hrow < c.hist_cap) ? hrow : -1;
@@ -1481,14 +1500,14 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   for (int j = 0; j < 2 && j < m; ++j) {  // counts of trees 0 and 1
     mbar_wait(&S.cnt_mbar[j & 1], par2(j));
     counts_add(c, X, S, j, G.hdr[j].nslots, lane);
-    if (X.fwd) forward_counts(c, X, S, j, G.hdr[j].nslots, lane);
+    if (X.fwd) forward_counts(c, X, G, j, G.hdr[j].nslots, lane);
   }
   if (m > 0) prepare_tree(0);
   for (int e = 0; e <= m; ++e) {
     if (e + 2 < m) {  // B_e done: publish the counts of tree e+2
       mbar_wait(&S.cnt_mbar[e & 1], par2(e + 2));
       counts_add(c, X, S, e + 2, G.hdr[e + 2].nslots, lane);
-      if (X.fwd) forward_counts(c, X, S, e + 2, G.hdr[e + 2].nslots, lane);
+      if (X.fwd) forward_counts(c, X, G, e + 2, G.hdr[e + 2].nslots, lane);
     }
     // tree e+1's count-only terms: prep[(e+1)&1] was last read by decide(e-1)
     // and decide_post(e-1), both done
@@ -1507,9 +1526,9 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
     }
     if (e == m && X.fwd) {  // two-level: this forwarder's stage baselines, for the next sweep
       const size_t g = (size_t)xgroup(c, G.cta);
-      const unsigned long long *src = &S.xsprev[0][0];
+      const unsigned long long *src = &G.hs->xsprev[0][0];
       for (int i = lane; i < kXSets * (int)kXPrevWords; i += 32) c.xssnap[g * kXSets * kXPrevWords + i] = src[i];
-      const unsigned long long *cs = &S.csprev[0][0];
+      const unsigned long long *cs = &G.hs->csprev[0][0];
       for (int i = lane; i < kCSets * (int)kCSetWords; i += 32) c.cssnap[g * kCSets * kCSetWords + i] = cs[i];
     }
     if (e == m && G.cta == 0) {  // the next sweep's exchange baselines
@@ -1523,7 +1542,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   }
 }
 
-template <int W>
+template <int W, bool HIER>
 __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SweepSmem &S = *reinterpret_cast<SweepSmem *>(smem_raw);
@@ -1535,6 +1554,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   G.ring = smem_raw + sizeof(SweepSmem) + ((((size_t)c.m * sizeof(TreeHdr)) + 15) & ~(size_t)15);
   G.row_bytes = (uint32_t)ring_row_bytes(c.chunk, W == 0);
   G.slot_bytes = (uint32_t)ring_slot_bytes(c.chunk, c.rstride, W == 0);
+  G.hs = HIER ? reinterpret_cast<HierSmem *>(G.ring + (((size_t)kRing * G.slot_bytes + 15) & ~(size_t)15)) : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   G.cta = blockIdx.x;
   G.nblk = gridDim.x;
@@ -1566,11 +1586,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
     for (int i = tid; i < kXSets * (int)kXPrevWords; i += kSweepThreads) dst[i] = c.xsnap[1 + i];
     unsigned long long *cd = &S.cprev[0][0];
     for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cd[i] = c.csnap[i];
-    if (c.hier && G.cta == xgroup(c, G.cta)) {  // two-level forwarder: its stage baselines
+    if (HIER && G.cta == xgroup(c, G.cta)) {  // two-level forwarder: its stage baselines
       const size_t g = (size_t)xgroup(c, G.cta);
-      unsigned long long *xs = &S.xsprev[0][0];
+      unsigned long long *xs = &G.hs->xsprev[0][0];
       for (int i = tid; i < kXSets * (int)kXPrevWords; i += kSweepThreads) xs[i] = c.xssnap[g * kXSets * kXPrevWords + i];
-      unsigned long long *cs = &S.csprev[0][0];
+      unsigned long long *cs = &G.hs->csprev[0][0];
       for (int i = tid; i < kCSets * (int)kCSetWords; i += kSweepThreads) cs[i] = c.cssnap[g * kCSets * kCSetWords + i];
     }
   }
@@ -1599,9 +1619,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
     K.lm_term = __dmul_rn(__dmul_rn(__dmul_rn(0.5, c.hp.leaf_mean), c.hp.leaf_mean), K.tau_mu);
     long long *tl = (BART_TIMELINE && c.timeline && G.cta == 0 && lane == 0) ? c.timeline : nullptr;
     if (warp == kCtrlWarp)
-      control_loop(c, S, G, lane, K, xbase, tl);
+      control_loop<HIER>(c, S, G, lane, K, xbase, tl);
     else
-      helper_loop(c, S, G, lane, K, xbase, tl);
+      helper_loop<HIER>(c, S, G, lane, K, xbase, tl);
   } else {
     long long *tl = (BART_TIMELINE && c.timeline && tid == 0 && G.cta == 0) ? c.timeline : nullptr;
     if constexpr (W == 0)
@@ -1612,15 +1632,17 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
 }
 
 typedef void (*SweepFn)(ChainDev);
-static SweepFn sweep_fn(int W) {
+template <bool HIER>
+static SweepFn sweep_fn_t(int W) {
   switch (W) {
-    case 0: return sweep_kernel<0>;
-    case 1: return sweep_kernel<1>;
-    case 2: return sweep_kernel<2>;
-    case 4: return sweep_kernel<4>;
-    default: return sweep_kernel<8>;
+    case 0: return sweep_kernel<0, HIER>;
+    case 1: return sweep_kernel<1, HIER>;
+    case 2: return sweep_kernel<2, HIER>;
+    case 4: return sweep_kernel<4, HIER>;
+    default: return sweep_kernel<8, HIER>;
   }
 }
+static SweepFn sweep_fn(int W, bool hier = false) { return hier ? sweep_fn_t<true>(W) : sweep_fn_t<false>(W); }
 
 int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -1647,18 +1669,19 @@ int sweep_launch(const ChainDev &c, size_t smem, cudaStream_t s) {
     attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.numAttrs = 2;
   }
-  return (int)cudaLaunchKernelEx(&cfg, sweep_fn(c.stream ? 0 : sweep_words_per_thread(c.chunk)), c);
+  return (int)cudaLaunchKernelEx(&cfg, sweep_fn(c.stream ? 0 : sweep_words_per_thread(c.chunk), c.hier != 0), c);
 }
 
 cudaError_t sweep_prepare(size_t smem) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  for (int W : {0, 1, 2, 4, 8}) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_fn(W), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         optin > (int)smem ? optin : (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  for (int W : {0, 1, 2, 4, 8})
+    for (bool hier : {false, true}) {
+      cudaError_t e = cudaFuncSetAttribute(sweep_fn(W, hier), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           optin > (int)smem ? optin : (int)smem);
+      if (e != cudaSuccess) return e;
+    }
   return cudaSuccess;
 }
 

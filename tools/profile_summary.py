@@ -37,7 +37,11 @@ H, U, V = r[0], r[1], r[2]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
-        "smsp__warp_issue_stalled_barrier_per_warp_active.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "smsp__warp_issue_stalled_barrier_per_warp_active.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"]
 m = {k: (V[H.index(k)], U[H.index(k)]) for k in want if k in H}
 
 
@@ -52,8 +56,10 @@ n, mm = bench["config"]["n"], bench["config"]["ntree"]
 dram = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
 summary = {
     "kernel": "bart::sweep_kernel<4> (one MCMC iteration: in-kernel proposals + sequential tree sweep + sigma)",
-    "command": "ncu --set full --clock-control none --import-source on -k regex:sweep -s 3 -c 1 "
-               "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu",
+    "command": "ncu --set full --clock-control none --import-source on -k regex:sweep -s 203 -c 1 "
+               "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu  (launch 203: after the 200-iteration "
+               "burn-in and 3 warm-up steps, i.e. at steady state)",
+    "trees_at_capture": bench.get("trees"),
     "workload": bench["config"]["workload"],
     "duration_us_ncu": float(m["gpu__time_duration.sum"][0]) * (1e3 if m["gpu__time_duration.sum"][1] == "ms" else 1),
     "dram_bytes_per_launch": dram,
