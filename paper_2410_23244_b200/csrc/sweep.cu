@@ -281,7 +281,9 @@ __device__ __forceinline__ void store_warp_sums(const double (&acc)[C > 0 ? C : 
     const double v = warp_xreduce<V, 4>(vals, lane, idx);
     if ((lane & xreduce_group_mask(V)) == 0) {
       const int slot = idx < C ? base + idx : A.ns - 1;
-      if (idx < V && (idx >= C || base + idx < A.ns)) S.wsum[warp][slot] = v;
+      // compared slots beyond the tree's (padded variants) are not stored: with
+      // TOTAL, slot ns-1 is the running total's, and only it may write there
+      if (idx < V && (idx >= C || base + idx < (TOTAL ? A.ns - 1 : A.ns))) S.wsum[warp][slot] = v;
     }
     TL_STAMP(ts && TOTAL) ts[25] = gtimer_after(v);
   }
@@ -349,25 +351,34 @@ __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)
     for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
     return;
   }
+  // compared-slot variants: each is a fully unrolled pass over the W words,
+  // so every variant is instruction-cache footprint the next tree may miss
+  // (ncu: no_instruction stalls ~16% of samples); BART_SUMS_SET trades
+  // compared slots (~300 cycles each, tools/apass_bench.cu) against variants:
+  //   3: one variant per width 1..8   2: {1,2,3,4,6,8}   1: {1,2,3,4,8}   0: {1,2,4,8}
+#ifndef BART_SUMS_SET
+#define BART_SUMS_SET 3
+#endif
   switch (A.ns) {
     case 1: sums_pass<W, 0, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
     case 2: sums_pass<W, 1, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+#if BART_SUMS_SET >= 1
     case 3: sums_pass<W, 2, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
-    case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
-#ifndef BART_SUMS_WIDE_VARIANTS
-#define BART_SUMS_WIDE_VARIANTS 1
+#else
+    case 3:
 #endif
-#if BART_SUMS_WIDE_VARIANTS
-    // one variant per width: a compared slot costs ~300 cycles per pass
-    // (tools/apass_bench.cu), more than the variants' instruction-cache cost
+    case 4: sums_pass<W, 3, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+#if BART_SUMS_SET >= 3
     case 5: sums_pass<W, 4, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
     case 6: sums_pass<W, 5, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
     case 7: sums_pass<W, 6, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
-    case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+#elif BART_SUMS_SET == 2
+    case 5: case 6: sums_pass<W, 5, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 7:
 #else
-    case 5: case 6: case 7: case 8:
-      sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
+    case 5: case 6: case 7:
 #endif
+    case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
     default:
       sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
       for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);

@@ -34,8 +34,9 @@ def main():
             d = json.loads(out.stdout.strip().splitlines()[-1])
             fk = d.get("forest_kernels") or {}
             fs = "  ".join(f"{k} {v['ms'] * 1e3:6.1f}us" for k, v in fk.items() if isinstance(v, dict))
-            print(f"{name:24s} {d['value']:9.1f} {d['unit']}  e2e {d['e2e']['value']:8.1f}  ms {d['ms_per_step']:.4f}  {fs}",
-                  flush=True)
+            tr = (d.get("trees") or {}).get("mean_leaves")
+            print(f"{name:24s} {d['value']:9.1f} {d['unit']}  e2e {d['e2e']['value']:8.1f}  ms {d['ms_per_step']:.4f}  "
+                  f"leaves {tr}  {fs}", flush=True)
         except Exception:
             print(name, "FAILED", out.stdout[-500:], out.stderr[-2000:], flush=True)
 
