@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--p", type=int, default=100)
     ap.add_argument("--m", type=int, default=200)
     ap.add_argument("--depth", type=int, default=6)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=CPU_TIMED_STEPS)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
