@@ -110,10 +110,11 @@ struct bart_chain {
   TraceState tr;
   uint8_t *result_stage = nullptr;  // pinned: last_accepted (m) + sigma2
   // bart_step pipeline, two slots (slot = iteration % 2): the injected random
-  // block goes host (pinned stage) -> device block on h2d, overlapping the
-  // previous step's kernel; the step's accept flags and sigma2 draw go to
-  // per-slot device buffers and come back on d2h into pinned step_out, so the
-  // host reads step k after launching step k+1.
+  // block is written into the slot's pinned stage, which the step kernel
+  // reads directly (zero-copy) while the host prepares the next step; the
+  // step's accept flags and sigma2 draw go to per-slot device buffers and come
+  // back on d2h into pinned step_out, so the host reads step k after
+  // launching step k+1.
   double *rstage[2] = {nullptr, nullptr};
   double *rblock[2] = {nullptr, nullptr};
   uint8_t *acc_slot[2] = {nullptr, nullptr};
@@ -122,9 +123,8 @@ struct bart_chain {
   double *res_sdraw = nullptr;
   double *res_block = nullptr;  // the random block (StepRandoms) the latest step consumed
   uint8_t *step_out = nullptr;
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t copy_done[2] = {nullptr, nullptr}, kernel_done[2] = {nullptr, nullptr},
-              step_out_ready[2] = {nullptr, nullptr};
+  cudaStream_t d2h = nullptr;
+  cudaEvent_t kernel_done[2] = {nullptr, nullptr}, step_out_ready[2] = {nullptr, nullptr};
   bool update_sigma = true;
   cudaGraphExec_t graph_step[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][injected randoms]
   int64_t slot_iter[2] = {-1, -1};  // which iteration each result slot holds
@@ -153,18 +153,15 @@ void free_chain(bart_chain *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   // a stream-mode chain pinned its residuals in L2: release the persisting lines
   if (h->c.persist_bytes > 0) cudaCtxResetPersistingL2Cache();
-  if (h->h2d) cudaStreamSynchronize(h->h2d);
   if (h->d2h) cudaStreamSynchronize(h->d2h);
   for (auto *p : h->rstage)
     if (p) cudaFreeHost(p);
   if (h->result_stage) cudaFreeHost(h->result_stage);
   if (h->step_out) cudaFreeHost(h->step_out);
   for (int k = 0; k < 2; ++k) {
-    if (h->copy_done[k]) cudaEventDestroy(h->copy_done[k]);
     if (h->kernel_done[k]) cudaEventDestroy(h->kernel_done[k]);
     if (h->step_out_ready[k]) cudaEventDestroy(h->step_out_ready[k]);
   }
-  if (h->h2d) cudaStreamDestroy(h->h2d);
   if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -867,11 +864,9 @@ static cudaError_t ensure_step_pipeline(bart_chain *h) {
   if (e == cudaSuccess) e = own(h, &h->sdraw_slot[1], 1);
   if (e == cudaSuccess) e = own(h, &h->acc_slot[1], (size_t)c.m);
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaMallocHost(&h->rstage[k], rwords * 8);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
-    e = cudaEventCreateWithFlags(&h->copy_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
+    e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // the new buffers' zero fill
@@ -888,8 +883,14 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   CUDA_TRY(ensure_step_pipeline(h));
   const int slot = (int)(h->iteration & 1);
   ChainDev args = step_args(h, rnd ? 0 : 1);
-  double *blk = h->rblock[slot];
   const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
+  // injected randoms: the kernel reads the block straight from the slot's
+  // pinned stage (zero-copy over the host link: the block's 8(6m + m*2^D) + 8
+  // bytes are the step's host->device transfer, with no copy-engine hop and
+  // no cross-stream event between the copy and the kernel); device randoms:
+  // the slot's device block, which the kernel writes
+  double *blk = h->rblock[slot];
+  if (rnd) CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&blk), h->rstage[slot], 0));
   args.rand_move = blk;
   args.rand_acc = blk + nm;
   args.rand_z = blk + nm + na;
@@ -898,21 +899,16 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   args.sigma2_draw = h->sdraw_slot[slot];
   if (rnd) {
     if (!rnd->move_u || !rnd->accept_u || !rnd->leaf_z) return fail(BART_EINVAL, "incomplete randoms");
-    // the slot's pinned stage is free once its last copy ran; its device block
-    // once the step two back (which read it) is done and its result is read out
-    CUDA_TRY(cudaEventSynchronize(h->copy_done[slot]));
+    // the slot's stage is free once the step two back, which read it, is done
+    CUDA_TRY(cudaEventSynchronize(h->kernel_done[slot]));
     double *st = h->rstage[slot];
     std::memcpy(st, rnd->move_u, nm * 8);
     std::memcpy(st + nm, rnd->accept_u, na * 8);
     std::memcpy(st + nm + na, rnd->leaf_z, nz * 8);
     st[nm + na + nz] = rnd->chi2;
-    CUDA_TRY(cudaStreamWaitEvent(h->h2d, h->step_out_ready[slot], 0));
-    CUDA_TRY(cudaMemcpyAsync(blk, st, (nm + na + nz + 1) * 8, cudaMemcpyHostToDevice, h->h2d));
-    CUDA_TRY(cudaEventRecord(h->copy_done[slot], h->h2d));
-    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->copy_done[slot], 0));
-  } else {
-    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[slot], 0));
   }
+  // the slot's result buffers are free once the step two back was read out
+  CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[slot], 0));
   // one captured launch per (slot, randoms kind): graph replay skips the
   // cooperative launch's per-call validation
   cudaGraphExec_t &gx = h->graph_step[slot][rnd ? 1 : 0];
@@ -1079,11 +1075,11 @@ int bart_get_randoms(bart_chain *h, double *move_u, double *accept_u, double *le
   if (int rc = bart_sync(h)) return rc;
   const ChainDev &c = h->c;
   const size_t nm = (size_t)c.m * 5, na = (size_t)c.m, nz = (size_t)c.m * c.size;
-  const double *b = h->res_block;
-  if (move_u) CUDA_TRY(cudaMemcpy(move_u, b, nm * 8, cudaMemcpyDeviceToHost));
-  if (accept_u) CUDA_TRY(cudaMemcpy(accept_u, b + nm, na * 8, cudaMemcpyDeviceToHost));
-  if (leaf_z) CUDA_TRY(cudaMemcpy(leaf_z, b + nm + na, nz * 8, cudaMemcpyDeviceToHost));
-  if (chi2) CUDA_TRY(cudaMemcpy(chi2, b + nm + na + nz, 8, cudaMemcpyDeviceToHost));
+  const double *b = h->res_block;  // a device block, or (injected) a pinned stage
+  if (move_u) CUDA_TRY(cudaMemcpy(move_u, b, nm * 8, cudaMemcpyDefault));
+  if (accept_u) CUDA_TRY(cudaMemcpy(accept_u, b + nm, na * 8, cudaMemcpyDefault));
+  if (leaf_z) CUDA_TRY(cudaMemcpy(leaf_z, b + nm + na, nz * 8, cudaMemcpyDefault));
+  if (chi2) CUDA_TRY(cudaMemcpy(chi2, b + nm + na + nz, 8, cudaMemcpyDefault));
   return BART_OK;
 }
 

@@ -1482,6 +1482,9 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
   // trace row of this iteration (read before the sigma CTA bumps the counter)
   const int64_t hrow = c.acc_hist ? (int64_t)*c.iter_dev - c.hist_base : -1;
   const int64_t hist_row = (hrow >= 0 && hrow < c.hist_cap) ? hrow : -1;
+  // the step's chi-square draw, read now: an injected block lives in pinned
+  // host memory (one host-link round trip, off the sweep's tail)
+  const double chi2 = G.cta == c.m % G.nblk ? *c.rand_chi2 : 0.0;
   auto issue_tree = [&](int j) {  // lane 0: cache row, split column, record -> ring slot j % kRing
     const TreeHdr hd = G.hdr[j];
     unsigned long long *mb = &S.mbar[j % kRing];
@@ -1529,7 +1532,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
       decide_post(c, S, S.prep[e & 1], S.dec[e & 1], G.rec(e), G.hdr[e], e, lane, K, hist_row);
     if (e == m && G.cta == m % G.nblk && lane == 0) {  // sigma^2 (sampler.py:797-799, 906-908)
       const HP &hp = c.hp;
-      const double s2 = __ddiv_rn(__dadd_rn(__dmul_rn(hp.nu, hp.lam), S.tot_sum[0]), *c.rand_chi2);
+      const double s2 = __ddiv_rn(__dadd_rn(__dmul_rn(hp.nu, hp.lam), S.tot_sum[0]), chi2);
       *c.sigma2_draw = s2;
       if (hp.update_sigma) *c.sigma2 = s2;
       if (hist_row >= 0) c.sig_hist[hist_row] = hp.update_sigma ? s2 : *c.sigma2;

@@ -44,3 +44,17 @@ def reads():
 t_reads = timed(lambda: (st._cache.clear(), st.last_accepted, st.sigma2))
 print(f"n={n}: per step (us): host StepRandoms.draw {t_draw:.0f} | device step (graph, device RNG) {t_dev:.0f} | "
       f"step(randoms) {t_step:.0f} | full e2e {t_full:.0f} | accepted+sigma2 reads {t_reads:.0f}")
+
+
+def pipelined():  # bench.py's e2e loop: read step k-1 after launching step k
+    step(st, hp, rng=rng)
+    if st.iteration >= 2:
+        st.step_result(st.iteration - 2)
+
+
+t_pipe = timed(pipelined)
+def host_only():  # the host's share of one pipelined iteration, device work excluded
+    t0 = time.perf_counter()
+    StepRandoms.draw(rng, m, size, hp.nu + n)
+    return time.perf_counter() - t0
+print(f"pipelined e2e loop {t_pipe:.0f} us per step (device step {t_dev:.0f} us)")
