@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--burn", type=int, default=200,
                     help="iterations run before warm-up so the timed chain is at steady state")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--n", "--points", dest="n", type=int, default=1_000_000)  # --points: under torchrun (--n is ambiguous there)
     ap.add_argument("--p", type=int, default=100)
     ap.add_argument("--m", type=int, default=200)
     ap.add_argument("--depth", type=int, default=6)
@@ -228,8 +228,13 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
 
+        local = local % max(1, torch.cuda.device_count())  # one GPU per rank; several ranks per GPU only in tests
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: ranks sharing a GPU (test)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -239,7 +244,7 @@ def allreduce_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
