@@ -177,11 +177,6 @@ cudaError_t own(bart_chain *h, T **p, size_t count) {
   return e;
 }
 
-int reset_mailbox_if_needed(bart_chain *, int64_t) {
-  // the exchange accumulators and counter are monotonic and wrap safely mod 2^64
-  return BART_OK;
-}
-
 // One iteration = ONE launch: the sweep kernel proposes every tree first
 // (injected or device randoms), then sweeps.
 ChainDev step_args(const bart_chain *h, int device_rng) {
@@ -879,7 +874,6 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
   ChainDev &c = h->c;
-  if (int rc = reset_mailbox_if_needed(h, 1)) return rc;
   CUDA_TRY(ensure_step_pipeline(h));
   const int slot = (int)(h->iteration & 1);
   ChainDev args = step_args(h, rnd ? 0 : 1);
@@ -984,7 +978,6 @@ int bart_run(bart_chain *h, int64_t n_iter) {
   if (!h) return fail(BART_EINVAL, "NULL handle");
   if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
-  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   ensure_graph(h);
   for (int k = 0; k < 2; ++k)
     if (h->step_out_ready[k]) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
@@ -1338,7 +1331,6 @@ int bart_sum_leaf_values(const bart_dims *dims, const float *leaf_value, const u
 int bart_run_timed(bart_chain *h, int64_t n_iter, float *ms) {
   if (!h || !ms) return fail(BART_EINVAL, "NULL argument");
   CUDA_TRY(cudaSetDevice(h->device));
-  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   ensure_graph(h);
   cudaEvent_t a, b;
   CUDA_TRY(cudaEventCreate(&a));
@@ -1405,7 +1397,6 @@ int bart_profile_forest(bart_chain *h, int reps, float *ms) {
 int bart_profile(bart_chain *h, int64_t n_iter, float *ms) {
   if (!h || !ms) return fail(BART_EINVAL, "NULL argument");
   CUDA_TRY(cudaSetDevice(h->device));
-  if (int rc = reset_mailbox_if_needed(h, n_iter)) return rc;
   std::vector<cudaEvent_t> ev((size_t)(3 * n_iter + 2));
   for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventRecord(ev[0], h->stream));

@@ -157,16 +157,6 @@ __device__ __forceinline__ long long nstimer() {
 }
 
 // ------------------------------------------------------------ byte-lane ops
-// refresh_leaf_indices on 4 points: L==t -> 2t + (x >= cut) (sampler.py:541-545)
-__device__ __forceinline__ uint32_t grow4(uint32_t l, uint32_t x, uint32_t t, uint32_t cut) {
-  uint32_t out = 0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const uint32_t lb = (l >> (8 * b)) & 0xffu, xb = (x >> (8 * b)) & 0xffu;
-    out |= (lb == t ? 2u * t + (xb >= cut ? 1u : 0u) : lb) << (8 * b);
-  }
-  return out;
-}
 // collapse of a pruned pair back into its parent (sampler.py:755)
 __device__ __forceinline__ uint32_t collapse4(uint32_t l, uint32_t t) {
   uint32_t out = 0;
@@ -515,9 +505,6 @@ __device__ __forceinline__ void red_add(unsigned long long *p, unsigned long lon
     asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void ld_poll2(const unsigned long long *p, unsigned long long &a, unsigned long long &b) {
-  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
 // Kernel parameters the control and helper loops touch every tree, loaded
