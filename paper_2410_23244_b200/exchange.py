@@ -17,13 +17,20 @@ import math
 LIMB_BITS = 37
 LIMB_MASK = (1 << LIMB_BITS) - 1
 TOTAL_BITS = 3 * LIMB_BITS  # 111
-RANGE = 2.0 ** 45           # |partial| must stay below this (device flags BART error bit 0)
+RANGE = 2.0 ** 45           # single CTA: |partial| must stay below this (the device reports BART_ERANGE)
 
 
-def fixed_limbs(x: float) -> tuple[int, int, int]:
+def range_limit(ctas: int) -> float:
+    """The per-CTA bound: 2^46 / (CTAs over all shards, rounded up to a power of
+    two), so no total can wrap the 111-bit sum (sweep.cu xrange_limit)."""
+    bits = max(0, (int(ctas) - 1).bit_length())
+    return 2.0 ** (46 - bits)
+
+
+def fixed_limbs(x: float, limit: float = RANGE) -> tuple[int, int, int]:
     """to_limbs: hi = floor(x), lo = RN((x - hi) * 2^64); limbs of hi * 2^64 + lo."""
     x = float(x)
-    if not abs(x) < RANGE:
+    if not abs(x) < limit:
         raise OverflowError(f"partial {x} outside the exchange's fixed-point range")
     hi = math.floor(x)
     rem = x - float(hi)                 # exact
@@ -51,4 +58,21 @@ def exchange_total(partials) -> float:
     for x in partials:
         for k, limb in enumerate(fixed_limbs(x)):
             t[k] += limb
+    return limbs_total(*t)
+
+
+def two_level_total(shard_partials) -> float:
+    """The two-level exchange (bart_set_exchange): each shard's CTAs add into
+    the shard's stage words; the shard's forwarder adds the stage's limb sums,
+    once, into every shard's words.  The final words hold the same integers as
+    the flat exchange's, so the total is bit-identical (exchange_total of all
+    partials)."""
+    t = [0, 0, 0]
+    for partials in shard_partials:
+        stage = [0, 0, 0]
+        for x in partials:
+            for k, limb in enumerate(fixed_limbs(x)):
+                stage[k] += limb
+        for k in range(3):
+            t[k] += stage[k]  # the forwarder's one tagged add per word
     return limbs_total(*t)

@@ -16,7 +16,7 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-from paper_2410_23244_b200.exchange import exchange_total, fixed_limbs, limbs_total
+from paper_2410_23244_b200.exchange import exchange_total, fixed_limbs, limbs_total, range_limit, two_level_total
 from paper_2410_23244_b200.shard import ShardPlan, exchange_handles
 
 
@@ -37,6 +37,29 @@ def test_total_is_order_independent_and_exact():
         rng.shuffle(parts)
         assert exchange_total(parts) == t  # bit-identical in any arrival order
     assert abs(Fraction(t) - exact) <= abs(exact) * Fraction(2) ** -52 + Fraction(300) * Fraction(2) ** -64
+
+
+def test_two_level_total_equals_flat():
+    """Stage sums per shard, then one forwarded add per shard: the same integers
+    as every CTA adding into every shard's words."""
+    rng = np.random.default_rng(3)
+    parts = list(rng.normal(size=8 * 148) * 10.0 ** rng.integers(-3, 4, size=8 * 148))
+    flat = exchange_total(parts)
+    for shards in (1, 2, 3, 8):
+        cuts = np.sort(rng.choice(np.arange(1, len(parts)), shards - 1, replace=False)) if shards > 1 else []
+        split = np.split(np.array(parts), cuts)
+        assert two_level_total([list(p) for p in split]) == flat
+
+
+def test_range_limit_keeps_totals_from_wrapping():
+    assert range_limit(1) == 2.0 ** 46 and range_limit(148) == 2.0 ** 38 and range_limit(8 * 148) == 2.0 ** 35
+    for ctas in (1, 148, 1184):
+        lim = range_limit(ctas)
+        x = np.nextafter(lim, 0)
+        assert limbs_total(*[ctas * l for l in fixed_limbs(x, lim)]) == pytest.approx(ctas * x, rel=1e-15)
+        assert limbs_total(*[ctas * l for l in fixed_limbs(-x, lim)]) == pytest.approx(-ctas * x, rel=1e-15)
+        with pytest.raises(OverflowError):
+            fixed_limbs(lim, lim)
 
 
 def test_shard_plan_covers_points_contiguously():
