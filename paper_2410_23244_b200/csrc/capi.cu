@@ -112,19 +112,18 @@ struct bart_chain {
   // bart_step pipeline, two slots (slot = iteration % 2): the injected random
   // block is written into the slot's pinned stage, which the step kernel
   // reads directly (zero-copy) while the host prepares the next step; the
-  // step's accept flags and sigma2 draw go to per-slot device buffers and come
-  // back on d2h into pinned step_out, so the host reads step k after
-  // launching step k+1.
+  // kernel writes the step's accept flags, sigma2 draw and error flag straight
+  // into the slot's pinned step_out, so the host reads step k after launching
+  // step k+1 -- no copy engine, no second stream, no cross-stream event.
   double *rstage[2] = {nullptr, nullptr};
   double *rblock[2] = {nullptr, nullptr};
-  uint8_t *acc_slot[2] = {nullptr, nullptr};
-  double *sdraw_slot[2] = {nullptr, nullptr};
+  uint8_t *acc_base = nullptr;  // the chain's device result buffers (bart_run's graph writes them)
+  double *sdraw_base = nullptr;
   uint8_t *res_acc = nullptr;  // where the latest step's accept flags are
   double *res_sdraw = nullptr;
   double *res_block = nullptr;  // the random block (StepRandoms) the latest step consumed
   uint8_t *step_out = nullptr;
-  cudaStream_t d2h = nullptr;
-  cudaEvent_t kernel_done[2] = {nullptr, nullptr}, step_out_ready[2] = {nullptr, nullptr};
+  cudaEvent_t kernel_done[2] = {nullptr, nullptr};
   bool update_sigma = true;
   cudaGraphExec_t graph_step[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][injected randoms]
   int64_t slot_iter[2] = {-1, -1};  // which iteration each result slot holds
@@ -153,16 +152,13 @@ void free_chain(bart_chain *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   // a stream-mode chain pinned its residuals in L2: release the persisting lines
   if (h->c.persist_bytes > 0) cudaCtxResetPersistingL2Cache();
-  if (h->d2h) cudaStreamSynchronize(h->d2h);
   for (auto *p : h->rstage)
     if (p) cudaFreeHost(p);
   if (h->result_stage) cudaFreeHost(h->result_stage);
   if (h->step_out) cudaFreeHost(h->step_out);
   for (int k = 0; k < 2; ++k) {
     if (h->kernel_done[k]) cudaEventDestroy(h->kernel_done[k]);
-    if (h->step_out_ready[k]) cudaEventDestroy(h->step_out_ready[k]);
   }
-  if (h->d2h) cudaStreamDestroy(h->d2h);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -379,8 +375,8 @@ static int create_impl(const bart_dims *dims, int64_t n_total, int shard, int n_
   c.sigma2 = s2;
   c.sigma2_draw = s2d;
   c.accepted = acc;
-  h->acc_slot[0] = acc;
-  h->sdraw_slot[0] = s2d;
+  h->acc_base = acc;
+  h->sdraw_base = s2d;
   h->res_acc = acc;
   h->res_sdraw = s2d;
   h->res_block = rm;
@@ -856,16 +852,12 @@ static cudaError_t ensure_step_pipeline(bart_chain *h) {
   const ChainDev &c = h->c;
   const size_t rwords = (size_t)c.m * 5 + (size_t)c.m + (size_t)c.m * c.size + 1;
   cudaError_t e = own(h, &h->rblock[1], rwords);
-  if (e == cudaSuccess) e = own(h, &h->sdraw_slot[1], 1);
-  if (e == cudaSuccess) e = own(h, &h->acc_slot[1], (size_t)c.m);
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaMallocHost(&h->rstage[k], rwords * 8);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaHostAlloc(&h->rstage[k], rwords * 8, cudaHostAllocMapped);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k)
     e = cudaEventCreateWithFlags(&h->kernel_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->step_out_ready[k], cudaEventDisableTiming);
-  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // the new buffers' zero fill
-  if (e == cudaSuccess) e = cudaMallocHost(&h->step_out, 2 * step_out_stride(c.m));
+  if (e == cudaSuccess) e = cudaHostAlloc(&h->step_out, 2 * step_out_stride(c.m), cudaHostAllocMapped);
+  if (e == cudaSuccess) std::memset(h->step_out, 0, 2 * step_out_stride(c.m));
   return e;
 }
 
@@ -889,11 +881,16 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   args.rand_acc = blk + nm;
   args.rand_z = blk + nm + na;
   args.rand_chi2 = blk + nm + na + nz;
-  args.accepted = h->acc_slot[slot];
-  args.sigma2_draw = h->sdraw_slot[slot];
+  // the step's result, written by the kernel into the slot's pinned step_out
+  const size_t stride = step_out_stride(c.m);
+  uint8_t *out_host = h->step_out + (size_t)slot * stride, *out_dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&out_dev), out_host, 0));
+  args.accepted = out_dev;
+  args.sigma2_draw = reinterpret_cast<double *>(out_dev + stride - 16);
+  args.err_out = reinterpret_cast<int *>(out_dev + stride - 8);
   if (rnd) {
     if (!rnd->move_u || !rnd->accept_u || !rnd->leaf_z) return fail(BART_EINVAL, "incomplete randoms");
-    // the slot's stage is free once the step two back, which read it, is done
+    // the slot's stage (and result) is free once the step two back is done
     CUDA_TRY(cudaEventSynchronize(h->kernel_done[slot]));
     double *st = h->rstage[slot];
     std::memcpy(st, rnd->move_u, nm * 8);
@@ -901,8 +898,6 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
     std::memcpy(st + nm + na, rnd->leaf_z, nz * 8);
     st[nm + na + nz] = rnd->chi2;
   }
-  // the slot's result buffers are free once the step two back was read out
-  CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[slot], 0));
   // one captured launch per (slot, randoms kind): graph replay skips the
   // cooperative launch's per-call validation
   cudaGraphExec_t &gx = h->graph_step[slot][rnd ? 1 : 0];
@@ -923,19 +918,10 @@ int bart_step(bart_chain *h, const bart_randoms *rnd) {
   h->launches += 1;
   h->iteration += 1;
   CUDA_TRY(cudaEventRecord(h->kernel_done[slot], h->stream));
-  h->res_acc = h->acc_slot[slot];
-  h->res_sdraw = h->sdraw_slot[slot];
+  h->res_acc = out_host;
+  h->res_sdraw = reinterpret_cast<double *>(out_host + stride - 16);
   h->res_block = blk;
-  // this step's result -> pinned step_out[slot] on d2h, behind the step
-  const int64_t it = h->iteration - 1;
-  const size_t stride = step_out_stride(c.m);
-  uint8_t *dst = h->step_out + (size_t)slot * stride;
-  CUDA_TRY(cudaStreamWaitEvent(h->d2h, h->kernel_done[slot], 0));
-  CUDA_TRY(cudaMemcpyAsync(dst, h->acc_slot[slot], (size_t)c.m, cudaMemcpyDeviceToHost, h->d2h));
-  CUDA_TRY(cudaMemcpyAsync(dst + stride - 16, h->sdraw_slot[slot], 8, cudaMemcpyDeviceToHost, h->d2h));
-  CUDA_TRY(cudaMemcpyAsync(dst + stride - 8, c.err, 4, cudaMemcpyDeviceToHost, h->d2h));
-  CUDA_TRY(cudaEventRecord(h->step_out_ready[slot], h->d2h));
-  h->slot_iter[slot] = it;
+  h->slot_iter[slot] = h->iteration - 1;
   return BART_OK;
 }
 
@@ -946,7 +932,7 @@ int bart_read_step_result(bart_chain *h, int64_t iteration, uint8_t *accepted, d
   if (!h->step_out || h->slot_iter[iteration & 1] != iteration)
     return fail(BART_ESTATE, "iteration " + std::to_string(iteration) + " did not run through bart_step");
   CUDA_TRY(cudaSetDevice(h->device));
-  CUDA_TRY(cudaEventSynchronize(h->step_out_ready[iteration & 1]));
+  CUDA_TRY(cudaEventSynchronize(h->kernel_done[iteration & 1]));
   const size_t stride = step_out_stride(h->c.m);
   const uint8_t *src = h->step_out + (size_t)(iteration & 1) * stride;
   int err = 0;
@@ -979,10 +965,8 @@ int bart_run(bart_chain *h, int64_t n_iter) {
   if (h->shard_pending) return fail(BART_ESTATE, "shard not connected (bart_shard_connect)");
   CUDA_TRY(cudaSetDevice(h->device));
   ensure_graph(h);
-  for (int k = 0; k < 2; ++k)
-    if (h->step_out_ready[k]) CUDA_TRY(cudaStreamWaitEvent(h->stream, h->step_out_ready[k], 0));
-  h->res_acc = h->acc_slot[0];  // the graph's kernels use the base (slot 0) buffers
-  h->res_sdraw = h->sdraw_slot[0];
+  h->res_acc = h->acc_base;  // the graph's kernels use the base buffers
+  h->res_sdraw = h->sdraw_base;
   h->res_block = h->rblock[0];
   for (int64_t i = 0; i < n_iter; ++i) {
     if (h->graph) {
@@ -1045,7 +1029,7 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
   if (!h->result_stage) CUDA_TRY(cudaMallocHost(&h->result_stage, m + 24));
   uint8_t *st = h->result_stage;
   const size_t m8 = (m + 7) & ~(size_t)7;
-  if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->res_acc, m, cudaMemcpyDeviceToHost, h->stream));
+  if (accepted) CUDA_TRY(cudaMemcpyAsync(st, h->res_acc, m, cudaMemcpyDefault, h->stream));
   if (sigma2) CUDA_TRY(cudaMemcpyAsync(st + m8, h->c.sigma2, 8, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaMemcpyAsync(st + m8 + 8, h->c.err, 4, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1060,7 +1044,7 @@ int bart_get_step_result(bart_chain *h, uint8_t *accepted, double *sigma2) {
 
 int bart_get_accepted(bart_chain *h, uint8_t *out) {
   if (int rc = bart_sync(h)) return rc;
-  CUDA_TRY(cudaMemcpy(out, h->res_acc, (size_t)h->c.m, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, h->res_acc, (size_t)h->c.m, cudaMemcpyDefault));
   return BART_OK;
 }
 

@@ -112,6 +112,7 @@ struct ChainDev {
                                 // when one launch emulates several shards on one device)
   int64_t n_total;              // points of the whole chain (chi-square df, sampler.py:259)
   int *err;                     // device error flags (bit 0: exchange value out of fixed-point range)
+  int *err_out;                 // bart_step: the sigma CTA copies *err here at the end (pinned host), or null
   unsigned long long *xsnap;    // [1 + kXSets*kXPrevWords]: exchange count, then every polled
                                 // word's last complete value (the next sweep's baseline)
   unsigned long long *cacc;     // this shard's count channel [kCSets][kCSetWords] (polled)

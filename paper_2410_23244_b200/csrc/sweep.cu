@@ -1524,6 +1524,7 @@ __device__ __forceinline__ void helper_loop(const ChainDev &c, SweepSmem &S, con
       if (hp.update_sigma) *c.sigma2 = s2;
       if (hist_row >= 0) c.sig_hist[hist_row] = hp.update_sigma ? s2 : *c.sigma2;
       *c.iter_dev += 1ull;
+      if (c.err_out) *c.err_out = *reinterpret_cast<volatile int *>(c.err);  // with the step's result (host)
     }
     if (e == m && X.fwd) {  // two-level: this forwarder's stage baselines, for the next sweep
       const size_t g = (size_t)xgroup(c, G.cta);
