@@ -26,12 +26,12 @@ from oracle.bart_oracle import OracleChain
 pytestmark = pytest.mark.gpu
 
 
-def _burned_pair(n, p, m, burn, seed, groups=1, exchange="flat"):
+def _burned_pair(n, p, m, burn, seed, groups=1, exchange="flat", **fit_kw):
     from paper_2410_23244_b200.dgp import friedman1_binned
     from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
     from paper_2410_23244_b200.sampler import DeviceRNG, init_state, run
     Xq, y, _, grid = friedman1_binned(n, p, seed=seed)
-    hp, ys = derive_hyperparams(y, FitConfig(n_trees=m))
+    hp, ys = derive_hyperparams(y, FitConfig(n_trees=m, **fit_kw))
     y32 = ys.forward(y).astype(np.float32)
     st = init_state(Xq, grid.counts, y32, hp, DeviceRNG(seed + 100))
     if groups > 1:
@@ -111,4 +111,25 @@ def test_eight_copy_groups_at_shard_shape(exchange):
     cfg = st.sweep_config()
     assert cfg["ctas"] == 148 and _words(cfg["chunk"]) == 8
     _compare_steps(st, ora, hp, n, 3, seed=8)
+    st.close()
+
+
+def test_stream_mode_at_stream_size_matches_oracle():
+    """n = 2.5e6 exceeds the register budget (2.1M points per GPU), so the
+    sweep runs in stream mode by itself -- residuals in L2, refreshed rows in
+    the Lref ring -- the mode n=1e7 on 1-4 GPUs uses."""
+    st, ora, hp, n = _burned_pair(2_500_000, 20, 60, 30, seed=12)
+    assert st.sweep_config()["stream"] and st.sweep_config()["ctas"] == 148
+    _compare_steps(st, ora, hp, n, 2, seed=9)
+    st.close()
+
+
+def test_deep_wide_trees_match_oracle():
+    """D = 8 (256-slot leaf rows) with a prior that grows deep, bushy trees:
+    after burn-in some trees' larger trees have more than 8 leaves (the A
+    pass's multi-pass sums) and the decision's wide path; 148 CTAs."""
+    st, ora, hp, n = _burned_pair(600_000, 10, 40, 150, seed=21, max_depth=8, alpha=0.99, beta=0.3)
+    leaves = (st.forest.cutpoint > 0).sum(axis=1) + 1
+    assert leaves.max() > 8, leaves.max()
+    _compare_steps(st, ora, hp, n, 3, seed=10)
     st.close()
