@@ -25,7 +25,6 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass
-from typing import Optional
 
 import numpy as np
 

@@ -7,7 +7,6 @@
   with world_size 2 (the multi-GPU path's host protocol).
 """
 
-import math
 import os
 import socket
 import sys

@@ -79,7 +79,7 @@ SHAPES = {
 
 
 def _words(chunk):
-    from paper_2410_23244_b200.sampler import SamplerState  # noqa: F401  (library loaded)
+    """sweep_words_per_thread (csrc/sweep.cu): words per worker thread, 14 worker warps."""
     words = (chunk + 3) // 4
     for w in (1, 2, 4, 8):
         if w * 14 * 32 >= words:

@@ -5,7 +5,6 @@ usage: python tools/e2e_breakdown.py [n] [steps]
 import os, sys, time
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2410_23244_b200 import _native as N
 from paper_2410_23244_b200.dgp import friedman1_binned
 from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
 from paper_2410_23244_b200.sampler import DeviceRNG, StepRandoms, init_state, run, step

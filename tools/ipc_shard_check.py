@@ -23,7 +23,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     import torch
     import torch.distributed as dist
-    from paper_2410_23244_b200 import _native as N
     from paper_2410_23244_b200.dgp import friedman1
     from paper_2410_23244_b200.grid import build_grid_uniform, quantize
     from paper_2410_23244_b200.regression import FitConfig, derive_hyperparams
