@@ -69,5 +69,22 @@ print("arrival skew (ns): last publish - first publish ", q(pub.max(1) - pub.min
 print("detection jitter (ns): last done - first done  ", q(done.max(1) - done.min(1)))
 print("exchange latency (ns): first done - last publish", q(done.min(1) - pub.max(1)))
 late = np.argmax(pub, axis=1)
-print("latest publisher CTA histogram (top 5):", np.bincount(late, minlength=nb).argsort()[::-1][:5])
+hist = np.bincount(late, minlength=nb)
+top = hist.argsort()[::-1][:5]
+print("latest publisher CTAs (top 5, share of trees):", [(int(c), round(float(hist[c]) / m, 2)) for c in top])
+# per-CTA systematics (ns, averaged over trees): when it published relative to
+# the first publisher; when it saw the exchange complete relative to the first
+# CTA that did; and its own A-pass-to-publish time (publish e - done e-1)
+lat_pub = (pub - pub.min(1, keepdims=True)).mean(0)
+lat_done = (done - done.min(1, keepdims=True)).mean(0)
+work = (pub[1:] - done[:-1]).mean(0)
+order = lat_pub.argsort()[::-1]
+print("per-CTA mean publish lateness (ns): max %.0f, median %.0f, min %.0f" % (lat_pub.max(), np.median(lat_pub), lat_pub.min()))
+print("per-CTA mean detection lateness (ns): max %.0f, median %.0f, min %.0f" % (lat_done.max(), np.median(lat_done), lat_done.min()))
+print("per-CTA done(e-1) -> publish(e) (ns): max %.0f, median %.0f, min %.0f" % (work.max(), np.median(work), work.min()))
+print("latest 8 CTAs: publish lateness / detection lateness / A-to-publish (ns):")
+for ci in order[:8]:
+    print(f"  CTA {ci:3d}: {lat_pub[ci]:6.0f} / {lat_done[ci]:6.0f} / {work[ci]:6.0f}")
+print("corr(publish lateness, detection lateness) = %.2f, corr(publish lateness, A-to-publish) = %.2f" % (
+    np.corrcoef(lat_pub, lat_done)[0, 1], np.corrcoef(lat_pub, work)[0, 1]))
 st.close()
