@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=CPU_TIMED_STEPS)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--max-ctas", type=int, default=0, help="cap the sweep's CTAs (0: one per SM)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: shard ONE chain's points across the ranks (in-kernel NVLink exchange, strong "
                          "scaling; BASELINE configs[3] with --n 10000000) instead of independent replicas")
@@ -299,7 +300,7 @@ def run_ours(args):
                                 float(np.var(y32, ddof=1)), torch_all_gather(), device=local)
     else:
         # replicas: every rank runs an independent chain of the full workload
-        st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local)
+        st = init_state(Xq, max_cuts, y32, hp, DeviceRNG(1000 + rank), device=local, max_ctas=args.max_ctas or None)
     cfg = st.sweep_config()
     # the round-1 protocol (5 warm-up, then 20 timed iterations of a fresh chain,
     # 1-2-leaf trees), kept for comparison; then on to steady state
