@@ -358,7 +358,7 @@ def run_ours(args):
     barrier(world)
     t0 = time.perf_counter()
     for k in range(args.e2e_steps):
-        step(st, hp, rng=rng)  # host StepRandoms, pinned H2D, launch
+        step(st, hp, rng=rng)  # host StepRandoms into the pinned stage, launch
         if k > 0:  # the previous step's result, read while this step runs
             acc_prev, s2_prev = st.step_result(st.iteration - 2)
     acc_last, s2_last = st.step_result()
@@ -387,10 +387,11 @@ def run_ours(args):
                                          if sharded else (f"{world} independent chains (replicas)" if world > 1
                                                           else "single chain, 1 GPU"))),
             "e2e": {"value": e2e, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "per step: sampler.step(state, hp, rng=numpy Generator) = host StepRandoms + one pinned "
-                            "H2D copy + launch; each step's accept flags + sigma2 come back by D2H into pinned memory "
-                            "and are read (state.step_result) after the next step is launched, so the host's draw "
-                            "for step k+1 overlaps the device's step k"},
+                    "path": "per step: sampler.step(state, hp, rng=numpy Generator) = host StepRandoms written into a "
+                            "pinned stage that the step kernel reads over the host link (zero-copy H2D) + launch; "
+                            "the kernel writes each step's accept flags + sigma2 into pinned host memory (zero-copy "
+                            "D2H), read (state.step_result) after the next step is launched, so the host's draw for "
+                            "step k+1 overlaps the device's step k"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": committed_traffic(),
                          "kernel": "sweep_kernel (the whole step: one launch per iteration)",
