@@ -7,13 +7,15 @@
 // Layout of the traverse / evaluate kernels: each thread owns 16 consecutive
 // points (one 16-byte vector of every X column and cache row) and walks all
 // trees.
-// A tree is applied node by node in heap order, SWAR over the 16 point bytes:
-// points at internal node t move to 2t + (x >= cut) -- equivalent to the
-// reference's per-point descent, since parents precede children in heap
-// order.  The warp finds the tree's internal nodes with one ballot per 32
-// heap slots and broadcasts (node, axis, cut) by shuffle, so X is read as one
-// coalesced 16-byte load per (internal node, thread) and the cache written as
-// one 16-byte store per (tree, thread).
+// A tree is applied node by node in heap order, SWAR over the 16 point bytes
+// (common.cuh swar_step, 11 integer ops per 4 points; the root, where every
+// point starts, in 5): points at internal node t move to 2t + (x >= cut) --
+// equivalent to the reference's per-point descent, since parents precede
+// children in heap order.  traverse: the warp finds the tree's internal nodes
+// with one ballot per 32 heap slots and broadcasts (node, axis, cut) by
+// shuffle; evaluate: from a per-block node list in shared memory.  X is read as
+// one coalesced 16-byte load per (internal node, thread) and the cache written
+// as one 16-byte store per (tree, thread).
 //   predict    trees.sum_leaf_values (trees.py:206-218): f64 accumulation in
 //              tree order, so cached and fresh-traversal predictions agree
 //              bit for bit with the reference.
@@ -107,30 +109,21 @@ void launch_fill_root(uint8_t *L, int m, int64_t n, int64_t n_pad, cudaStream_t 
   if (n_pad > n) cudaMemset2DAsync(L + n, (size_t)n_pad, 0, (size_t)(n_pad - n), (size_t)m, s);
 }
 
-// SWAR on 4 point bytes: high bit where bytes are equal; 0x01 where x >= cut
-__device__ __forceinline__ uint32_t swar_eq(uint32_t a, uint32_t b4) {
-  const uint32_t x = a ^ b4;
-  return ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
-}
-__device__ __forceinline__ uint32_t swar_geu(uint32_t x, uint32_t c4) {
-  const uint32_t de = ((x & 0x00ff00ffu) | 0x01000100u) - (c4 & 0x00ff00ffu);
-  const uint32_t dodd = (((x >> 8) & 0x00ff00ffu) | 0x01000100u) - ((c4 >> 8) & 0x00ff00ffu);
-  return ((de >> 8) & 0x00010001u) | (dodd & 0x01000100u);
-}
-__device__ __forceinline__ uint32_t swar_step(uint32_t l, uint32_t x, uint32_t t4, uint32_t c4, uint32_t b4) {
-  const uint32_t msk = (swar_eq(l, t4) >> 7) * 0xffu;
-  return (l & ~msk) | (msk & (b4 | swar_geu(x, c4)));
-}
-
 // K words (4K points) per thread: the X column / cache-row vector type
 template <int K> struct Vec;
 template <> struct Vec<1> { typedef uint32_t T; };
 template <> struct Vec<2> { typedef uint2 T; };
 template <> struct Vec<4> { typedef uint4 T; };
+template <> struct Vec<8> { typedef uint4 T; };  // (vload: two vectors)
 template <int K>
 __device__ __forceinline__ void vload(uint32_t (&w)[K], const uint8_t *p) {
-  const typename Vec<K>::T v = __ldg(reinterpret_cast<const typename Vec<K>::T *>(p));
-  memcpy(w, &v, sizeof(w));
+  if constexpr (K == 8) {  // two 16-byte vectors
+    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p)), b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+    w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+  } else {
+    const typename Vec<K>::T v = __ldg(reinterpret_cast<const typename Vec<K>::T *>(p));
+    memcpy(w, &v, sizeof(w));
+  }
 }
 template <int K>
 __device__ __forceinline__ void vstore(uint8_t *p, const uint32_t (&w)[K]) {
@@ -181,8 +174,13 @@ __device__ __forceinline__ void traverse_pts(uint32_t (&l)[K], const uint8_t *__
       for (int g = 0; g < kNodeBatch; ++g) {
         if (use[g] && live) {
           const uint32_t t4 = 0x01010101u * node[g], c4 = 0x01010101u * cv[g], b4 = 0x01010101u * (2u * node[g]);
+          if (node[g] == 1u) {  // the root (first in heap order): every point is there
 #pragma unroll
-          for (int k = 0; k < K; ++k) l[k] = swar_step(l[k], x[g][k], t4, c4, b4);
+            for (int k = 0; k < K; ++k) l[k] = swar_child(x[g][k], c4, c4 & 0x7f7f7f7fu, b4);
+          } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) l[k] = swar_step(l[k], x[g][k], t4, c4, b4);
+          }
         }
       }
     }
@@ -200,10 +198,6 @@ __device__ __forceinline__ void valid_pts(uint32_t (&v)[K], int64_t i0, int64_t 
 }
 
 constexpr int kTravWords = 4;  // 16 points per thread (tools: 8 measured 20% slower at n = 1e6)
-#ifndef BART_EVAL_WORDS
-#define BART_EVAL_WORDS 4
-#endif
-constexpr int kEvalWords = BART_EVAL_WORDS;  // fused evaluate: words (4 points) per thread
 constexpr int kTravTrees = 4;  // trees per traverse block (grid y)
 // leaf values staged in shared memory as f64, kLeafStage doubles per block
 // (the conversion once per leaf instead of once per point and tree)
@@ -242,8 +236,9 @@ void launch_traverse(const uint8_t *Xt, int64_t n, int64_t ld, int D, int half, 
 }
 
 // trees [j0, j0 + nt) of the leaf table -> shared memory as f64 (whole block)
-__device__ __forceinline__ int stage_leaves(double *s_leaf, const float *__restrict__ leaf, int j0, int m, int size) {
-  const int per = kLeafStage / size, nt = m - j0 < per ? m - j0 : per;
+__device__ __forceinline__ int stage_leaves(double *s_leaf, const float *__restrict__ leaf, int j0, int m, int size,
+                                            int cap = kLeafStage) {
+  const int per = kLeafStage / size < cap ? kLeafStage / size : cap, nt = m - j0 < per ? m - j0 : per;
   __syncthreads();  // the previous chunk is consumed
   for (int i = threadIdx.x; i < nt * size; i += blockDim.x) s_leaf[i] = (double)__ldg(leaf + (size_t)j0 * size + i);
   __syncthreads();
@@ -482,33 +477,133 @@ void launch_predict_cached(const uint8_t *L, int64_t n, int64_t ld, int m, int s
   predict_cached_kernel<<<grid_for(ld, 1), 256, 0, s>>>(L, n, ld, m, size, leaf, out);
 }
 
-// fused traverse + sum over all trees, without materialising the (m, n) cache
-__global__ void __launch_bounds__(256) evaluate_kernel(const uint8_t *__restrict__ Xt, int64_t n, int64_t ld, int half,
-                                                       int m, const uint16_t *__restrict__ axis,
-                                                       const uint8_t *__restrict__ cut,
-                                                       const float *__restrict__ leaf, double *__restrict__ out) {
-  constexpr int K = kEvalWords;
+// Fused traverse + sum over all trees, without materialising the (m, n)
+// cache.  A column's address depends only on the tree (axis of the node), never
+// on the data, so each chunk of trees is flattened into a shared-memory list of
+// internal nodes in (tree, heap) order -- one 32-bit entry: axis | last-of-tree
+// | cut | node -- and every thread keeps the loads of the next P entries in
+// flight while it applies the current one (no per-tree ballot / shuffle on the
+// path).  A tree with no internal node gets a no-op entry (node 0 matches no
+// point).  Leaf values are added per tree in ascending order (trees.py:206-
+// 218), so the result is bit-identical to traverse + sum_leaf_values.
+// Measured at n=1e6, m=200 (steady state): 4 words x 1 entry ahead 172 us;
+// 8 x 1 171; 4 x 2 185; 4 x 4 191; 2 x 8 213 (more loads in flight lose: the
+// kernel is ALU-bound on the SWAR steps, not waiting on L2).
+#ifndef BART_EVAL_PIPE
+#define BART_EVAL_PIPE 1
+#endif
+#ifndef BART_EVAL_PIPE_WORDS
+#define BART_EVAL_PIPE_WORDS 4
+#endif
+constexpr int kEvalPipe = BART_EVAL_PIPE;
+constexpr int kEvalPipeWords = BART_EVAL_PIPE_WORDS;
+constexpr int kNodeStage = 2048;  // >= trees per leaf chunk x entries per tree (64 x 31 at D = 6, 16 x 127 at D = 8)
+constexpr int kNodeTrees = 1024;  // trees per chunk (D = 1's 2048-tree leaf chunks are halved: static smem < 48 KB)
+constexpr uint32_t kEntryEnd = 1u << 15;
+
+__device__ __forceinline__ uint32_t make_entry(uint32_t node, uint32_t cutv, uint32_t ax, bool end) {
+  return (ax << 16) | (end ? kEntryEnd : 0u) | (cutv << 7) | node;
+}
+
+// the internal nodes of trees [j0, j0 + nt) -> s_nodes (whole block); returns the entry count
+__device__ __forceinline__ int stage_nodes(uint32_t *s_nodes, int *s_off, const uint8_t *__restrict__ cut,
+                                           const uint16_t *__restrict__ axis, int j0, int nt, int half) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int jj = warp; jj < nt; jj += nwarps) {  // entries per tree (>= 1)
+    const uint8_t *cj = cut + (size_t)(j0 + jj) * half;
+    int cnt = 0;
+    for (int base = 0; base < half; base += 32) {
+      const int t = base + lane;
+      cnt += __popc(__ballot_sync(0xffffffffu, t >= 1 && t < half && __ldg(cj + t) != 0));
+    }
+    if (lane == 0) s_off[jj + 1] = cnt > 0 ? cnt : 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan (nt <= 64 at D = 6; a serial scan is noise next to the chunk)
+    s_off[0] = 0;
+    for (int jj = 0; jj < nt; ++jj) s_off[jj + 1] += s_off[jj];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < nt; jj += nwarps) {
+    const uint8_t *cj = cut + (size_t)(j0 + jj) * half;
+    const uint16_t *aj = axis + (size_t)(j0 + jj) * half;
+    const int o = s_off[jj], last = s_off[jj + 1] - 1;
+    int k = o;
+    for (int base = 0; base < half; base += 32) {
+      const int t = base + lane;
+      const uint32_t ct = t < half ? __ldg(cj + t) : 0u;
+      const bool in = t >= 1 && ct != 0u;
+      const uint32_t msk = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int pos = k + __popc(msk & ((1u << lane) - 1u));
+        s_nodes[pos] = make_entry((uint32_t)t, ct, __ldg(aj + t), pos == last);
+      }
+      k += __popc(msk);
+    }
+    if (k == o && lane == 0) s_nodes[o] = make_entry(0u, 0u, 0u, true);  // no internal node: a no-op step
+  }
+  __syncthreads();
+  return s_off[nt];
+}
+
+template <int K, int P>
+__global__ void __launch_bounds__(256) evaluate_kernel(const uint8_t *__restrict__ Xt, int64_t n, int64_t ld,
+                                                            int half, int m, const uint16_t *__restrict__ axis,
+                                                            const uint8_t *__restrict__ cut,
+                                                            const float *__restrict__ leaf, double *__restrict__ out) {
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4 * K;
   const bool live = i0 < ld;
-  const int lane = threadIdx.x & 31, size = 2 * half;
-  // grid y: one forest of a stacked batch (forest f at axis/cut + f*m*half,
-  // leaf + f*m*size, out + f*n)
-  const size_t f = blockIdx.y;
+  const int size = 2 * half;
+  const size_t f = blockIdx.y;  // one forest of a stacked batch
   axis += f * (size_t)m * half;
   cut += f * (size_t)m * half;
   leaf += f * (size_t)m * size;
   out += f * (size_t)n;
   __shared__ double s_leaf[kLeafStage];
+  __shared__ uint32_t s_nodes[kNodeStage];
+  __shared__ int s_off[kNodeTrees + 1];
+  const uint8_t *xp = Xt + (live ? i0 : 0);
   double acc[4 * K];
 #pragma unroll
   for (int b = 0; b < 4 * K; ++b) acc[b] = 0.0;
-  uint32_t l[K];
   for (int j0 = 0; j0 < m;) {
-    const int nt = stage_leaves(s_leaf, leaf, j0, m, size);
-    for (int jj = 0; jj < nt; ++jj) {
-      const int j = j0 + jj;
-      traverse_pts<K>(l, Xt, ld, i0, live, cut + (size_t)j * half, axis + (size_t)j * half, half, lane);
-      if (live) add_leaves_s<K>(acc, l, s_leaf + (size_t)jj * size);
+    const int nt = stage_leaves(s_leaf, leaf, j0, m, size, kNodeTrees);
+    const int total = stage_nodes(s_nodes, s_off, cut, axis, j0, nt, half);
+    uint32_t xq[P][K];
+#pragma unroll
+    for (int g = 0; g < P; ++g)
+      if (g < total && live) vload<K>(xq[g], xp + (size_t)(s_nodes[g] >> 16) * ld);
+    uint32_t l[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) l[k] = 0x01010101u;
+    const double *row = s_leaf;
+    for (int e0 = 0; e0 < total; e0 += P) {
+#pragma unroll
+      for (int g = 0; g < P; ++g) {
+        const int e = e0 + g;
+        if (e < total) {  // warp-uniform
+          const uint32_t ent = s_nodes[e];
+          uint32_t x[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) x[k] = xq[g][k];
+          if (e + P < total && live) vload<K>(xq[g], xp + (size_t)(s_nodes[e + P] >> 16) * ld);
+          const uint32_t node = ent & 0x7fu, cv = (ent >> 7) & 0xffu;
+          const uint32_t t4 = 0x01010101u * node, c4 = 0x01010101u * cv, b4 = 0x01010101u * (2u * node);
+          if (node == 1u) {  // the root (a tree's first entry): every point is there
+#pragma unroll
+            for (int k = 0; k < K; ++k) l[k] = swar_child(x[k], c4, c4 & 0x7f7f7f7fu, b4);
+          } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) l[k] = swar_step(l[k], x[k], t4, c4, b4);
+          }
+          if (ent & kEntryEnd) {
+            if (live) add_leaves_s<K>(acc, l, row);
+            row += size;
+#pragma unroll
+            for (int k = 0; k < K; ++k) l[k] = 0x01010101u;
+          }
+        }
+      }
     }
     j0 += nt;
   }
@@ -524,8 +619,8 @@ void launch_evaluate_batch(const uint8_t *Xt, int64_t n, int64_t ld, int D, int 
                            const uint16_t *axis, const uint8_t *cut, const float *leaf, double *out, cudaStream_t s) {
   (void)D;
   if (n_forests <= 0 || n <= 0) return;
-  const dim3 grid(grid_for(ld, kEvalWords), (unsigned)n_forests);
-  evaluate_kernel<<<grid, 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, leaf, out);
+  const dim3 grid(grid_for(ld, kEvalPipeWords), (unsigned)n_forests);
+  evaluate_kernel<kEvalPipeWords, kEvalPipe><<<grid, 256, 0, s>>>(Xt, n, ld, half, m, axis, cut, leaf, out);
 }
 
 // r = f32(f64(y) - pred)  (tests/util.py:19-23 recomputation)
