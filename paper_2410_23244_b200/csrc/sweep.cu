@@ -1560,7 +1560,11 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(ChainDev c) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   G.cta = blockIdx.x;
   G.nblk = gridDim.x;
+#ifdef BART_CHUNK_ROT  // diagnostics: CTA c sweeps chunk (c + ROT) % nblk (tools/jobs/r02_rot.sh)
+  G.start = (int64_t)((G.cta + BART_CHUNK_ROT) % G.nblk) * G.chunk;
+#else
   G.start = (int64_t)G.cta * G.chunk;
+#endif
   const int len = (int)((c.n - G.start) < (int64_t)G.chunk ? (c.n - G.start) : (int64_t)G.chunk);
   G.lenp = (uint32_t)((len + 15) & ~15);
   G.nwords = (int)(G.lenp >> 2);
