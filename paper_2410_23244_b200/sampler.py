@@ -432,9 +432,10 @@ class SamplerState:
         """Record the current state as a kept draw (asynchronous)."""
         N.check(N.lib().bart_trace_keep(self._h))
 
-    def trace_read(self, train_draws: bool = True) -> dict:
+    def trace_read(self, train_draws: bool = True, train_out: np.ndarray | None = None) -> dict:
         """Everything recorded since trace_begin, in the reference's layouts (scaled units);
-        train_draws=False leaves the (n_keep, n) draws on the device (trace_read_draws)."""
+        train_draws=False leaves the (n_keep, n) draws on the device (trace_read_draws);
+        train_out: a C-contiguous (n_keep, n) float64 array to read the draws into."""
         ni, nk = C.c_int64(), C.c_int64()
         N.check(N.lib().bart_trace_counts(self._h, C.byref(ni), C.byref(nk)))
         ni, nk, n, m, D = ni.value, nk.value, self.y.size, self._m, self._D
@@ -442,7 +443,8 @@ class SamplerState:
         out = dict(
             accepted=np.empty((ni, m), np.uint8), sigma2_iter=np.empty(ni), sigma2_keep=np.empty(nk),
             train_mean=np.empty(n), train_var=np.empty(n),
-            train_draws=np.empty((nk, n)) if o["store_train"] and train_draws else None,
+            train_draws=(None if not (o["store_train"] and train_draws) else
+                         train_out if train_out is not None else np.empty((nk, n))),
             train_points=np.empty((nk, min(n, N.TRACE_POINTS))),
             test_draws=np.empty((nk, o["n_test"])) if o["n_test"] else None,
             mean_leaves=np.empty(nk),
