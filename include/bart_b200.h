@@ -264,6 +264,12 @@ int bart_sweep_config(bart_chain *h, int32_t *out /* [ctas, threads, chunk, smem
 int bart_grid_minmax(const double *X, int64_t n, int32_t p, double *lo, double *hi, int device);
 int bart_quantize(const double *X, int64_t n, int32_t p, const double *cutpoints, const int64_t *offsets,
                   uint8_t *out, int device);
+/* both for a uniform grid with X uploaded once (regression.fit's binning,
+ * regression.py:136 -> grid.py:77-95 + 121-134): lo / hi as bart_grid_minmax,
+ * the cutpoints lo + (hi - lo) * (k / (n_cutpoints + 1)), k = 1..n_cutpoints
+ * (none where lo == hi), and out as bart_quantize with them. */
+int bart_grid_uniform_quantize(const double *X, int64_t n, int32_t p, int32_t n_cutpoints, double *lo, double *hi,
+                               uint8_t *out, int device);
 
 const char *bart_last_error(void);
 const char *bart_version(void);

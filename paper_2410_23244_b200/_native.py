@@ -68,6 +68,7 @@ _SIGS = {
     "bart_trace_end": [_P],
     "bart_grid_minmax": [_P, C.c_int64, C.c_int32, _P, _P, C.c_int],
     "bart_quantize": [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_int],
+    "bart_grid_uniform_quantize": [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, C.c_int],
     "bart_set_state": [_P, _P, _P, _P, _P, _P, C.c_double],
     "bart_set_hparams": [_P, C.POINTER(HParams)],
     "bart_set_sigma2": [_P, C.c_double],

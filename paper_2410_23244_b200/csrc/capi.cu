@@ -774,6 +774,53 @@ int bart_quantize(const double *X, int64_t n, int32_t p, const double *cutpoints
   return BART_OK;
 }
 
+int bart_grid_uniform_quantize(const double *X, int64_t n, int32_t p, int32_t n_cutpoints, double *lo, double *hi,
+                               uint8_t *out, int device) {
+  if (!X || !lo || !hi || !out || n < 2 || p < 1) return fail(BART_EINVAL, "bad grid arguments");
+  if (n_cutpoints < 1 || n_cutpoints > 255) return fail(BART_EINVAL, "n_cutpoints must be in [1, 255]");
+  CUDA_TRY(cudaSetDevice(device));
+  DevBuf dx, keys, bad, dlo, dhi, dc, doff, dout;
+  CUDA_TRY(dx.alloc((size_t)n * p * 8));
+  CUDA_TRY(keys.alloc((size_t)2 * p * 8));
+  CUDA_TRY(bad.alloc(8));
+  CUDA_TRY(dlo.alloc((size_t)p * 8));
+  CUDA_TRY(dhi.alloc((size_t)p * 8));
+  CUDA_TRY(dc.alloc((size_t)p * n_cutpoints * 8));
+  CUDA_TRY(doff.alloc((size_t)(p + 1) * 8));
+  CUDA_TRY(dout.alloc((size_t)n * p));
+  CUDA_TRY(cudaMemcpy(dx.p, X, (size_t)n * p * 8, cudaMemcpyHostToDevice));
+  launch_minmax(dx.as<double>(), n, p, keys.as<long long>(), bad.as<unsigned long long>(), dlo.as<double>(),
+                dhi.as<double>(), 0);
+  unsigned long long nbad = 0;
+  CUDA_TRY(cudaMemcpy(&nbad, bad.p, 8, cudaMemcpyDeviceToHost));
+  if (nbad) return fail(BART_EINVAL, "predictors must be finite (" + std::to_string(nbad) + " non-finite values)");
+  CUDA_TRY(cudaMemcpy(lo, dlo.p, (size_t)p * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hi, dhi.p, (size_t)p * 8, cudaMemcpyDeviceToHost));
+  // the cutpoints as grid.build_grid_uniform computes them in numpy: frac_k =
+  // k / (K + 1) correctly rounded, then lo + (hi - lo) * frac_k, two roundings
+  // (x86-64 host code: no FMA contraction)
+  std::vector<double> cuts;
+  std::vector<int64_t> off(p + 1, 0);
+  cuts.reserve((size_t)p * n_cutpoints);
+  for (int a = 0; a < p; ++a) {
+    if (lo[a] != hi[a]) {
+      const double span = hi[a] - lo[a];
+      for (int k = 1; k <= n_cutpoints; ++k) {
+        const double frac = (double)k / (double)(n_cutpoints + 1);
+        const double step = span * frac;
+        cuts.push_back(lo[a] + step);
+      }
+    }
+    off[a + 1] = (int64_t)cuts.size();
+  }
+  if (!cuts.empty()) CUDA_TRY(cudaMemcpy(dc.p, cuts.data(), cuts.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(doff.p, off.data(), (size_t)(p + 1) * 8, cudaMemcpyHostToDevice));
+  launch_quantize(dx.as<double>(), n, p, dc.as<double>(), doff.as<int64_t>(), dout.as<uint8_t>(), 0);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, dout.p, (size_t)n * p, cudaMemcpyDeviceToHost));
+  return BART_OK;
+}
+
 int bart_destroy(bart_chain *h) {
   free_chain(h);
   return BART_OK;

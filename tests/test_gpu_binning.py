@@ -38,6 +38,28 @@ def test_uniform_grid_ranges_on_device():
         build_grid_uniform(X, 100, device=0)
 
 
+@pytest.mark.parametrize("nc", [1, 100, 255])
+def test_one_upload_grid_and_binning_equal_the_two_calls(nc):
+    """fit()'s binning (grid_uniform_quantize: X uploaded once, cutpoints from the
+    device ranges) equals build_grid_uniform + quantize, on the device and in
+    numpy, bit for bit -- including values exactly at cutpoints."""
+    from paper_2410_23244_b200.grid import build_grid_uniform, grid_uniform_quantize, quantize
+    rng = np.random.default_rng(nc)
+    X = rng.normal(size=(30011, 9)) * 10.0 ** rng.integers(-3, 4, size=9)
+    X[:, 4] = -1.25                                  # constant axis: no cutpoints
+    ref = build_grid_uniform(X, nc)
+    X[:nc, 0] = ref.cutpoints[0]                     # rows exactly at axis 0's cutpoints
+    ref = build_grid_uniform(X, nc)
+    grid, qm = grid_uniform_quantize(X, nc, 0)
+    for ca, cb in zip(ref.cutpoints, grid.cutpoints):
+        np.testing.assert_array_equal(ca, cb)
+    np.testing.assert_array_equal(qm.data, quantize(X, ref).data)
+    np.testing.assert_array_equal(qm.data, quantize(X, ref, device=0).data)
+    with pytest.raises(ValueError):
+        X[3, 2] = np.inf
+        grid_uniform_quantize(X, nc, 0)
+
+
 def _golden(name):
     import os
     return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
