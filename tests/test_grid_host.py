@@ -30,3 +30,4 @@ def test_host_quantize_non_finite_rows_match_reference():
     grid = build_grid_uniform(g["X"], 60)
     np.testing.assert_array_equal(grid.counts, g["counts"])
     np.testing.assert_array_equal(quantize(g["X_special"], grid).data, g["q_special"])
+
