@@ -229,9 +229,12 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
 
-        local = local % max(1, torch.cuda.device_count())  # one GPU per rank; several ranks per GPU only in tests
+        ndev = max(1, torch.cuda.device_count())
+        local = local % ndev  # one GPU per rank; several ranks per GPU only on a box with fewer GPUs
         torch.cuda.set_device(local)
-        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: ranks sharing a GPU (test)
+        # the bench's collectives carry only timings (no data path); NCCL refuses
+        # two ranks on one GPU, so ranks sharing GPUs use gloo
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl" if world <= ndev else "gloo")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
