@@ -5,18 +5,20 @@ Workload (default, BASELINE configs[2], the metric's config): gbart on
 synthetic Friedman #1 data, n=1e6, p=100, ntree=200, D=6, 100 uniform
 cutpoints.  A "step" is one full MCMC iteration (propose + sequential sweep
 over all 200 trees + sigma draw) on resident device state.  The chain is
-burned in (--burn, default 200 iterations, like the reference protocol's
-warm-up, bench.py:114-122) before the W warm-up and K timed steps, so the
-number is a steady-state one (trees at their posterior size, reported as
-"trees" in the line), not the 1-2-leaf trees of a fresh chain.
+burned in (--burn, default 2000 iterations; the reference's own protocol
+warms up 3, bench.py:114-122) before the W warm-up and K timed steps, so the
+number is a steady-state one: trees keep growing for ~1500 iterations
+(mean leaves 2.3 after 5, 3.7 after 200, 4.5-4.6 from ~1500 on, where the
+rate stops falling; tools/drift.py), reported as "trees" in the line.  The
+fresh-chain rate (iterations 5..25) is reported beside it.
 
   value     iterations/s of CUDA-graph-replayed device-RNG steps, CUDA events
             on the chain's stream, max over ranks; inputs (X 100 MB, leaf
             index 200 MB) exceed the 126 MB L2, no flush needed.
   e2e       the same metric through the reference-facing call
-            `step(state, hp, rng=numpy Generator)`: host StepRandoms draw,
-            H2D copy of that block, the step, and a D2H read of
-            last_accepted + sigma2 every step.
+            `step(state, hp, rng=numpy Generator)`: host StepRandoms draw
+            into the pinned stage the kernel reads (zero-copy H2D), the step,
+            and its accept flags + sigma2 read back (zero-copy D2H) every step.
   roofline  the sweep kernel: algorithmic bytes 10*n*m per launch (SURVEY.md
             §8d) / mean per-launch CUDA-event duration, vs measured HBM peak.
   cpu_baseline  the CPU oracle (numpy port of the reference, oracle/), one
@@ -55,7 +57,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--burn", type=int, default=200,
+    ap.add_argument("--burn", type=int, default=2000,
                     help="iterations run before warm-up so the timed chain is at steady state")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", "--points", dest="n", type=int, default=1_000_000)  # --points: under torchrun (--n is ambiguous there)

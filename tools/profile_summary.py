@@ -56,8 +56,8 @@ n, mm = bench["config"]["n"], bench["config"]["ntree"]
 dram = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
 summary = {
     "kernel": "bart::sweep_kernel<4> (one MCMC iteration: in-kernel proposals + sequential tree sweep + sigma)",
-    "command": "ncu --set full --clock-control none --import-source on -k regex:sweep -s 203 -c 1 "
-               "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu  (launch 203: after the 200-iteration "
+    "command": "ncu --set full --clock-control none --import-source on -k regex:sweep -s 2003 -c 1 "
+               "python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu  (launch 2003: after the 2000-iteration "
                "burn-in and 3 warm-up steps, i.e. at steady state)",
     "trees_at_capture": bench.get("trees"),
     "workload": bench["config"]["workload"],
