@@ -371,7 +371,15 @@ __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)
     case 8: sums_pass<W, 7, true, true>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0, ts); break;
     default:
       sums_pass<W, 8, true, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, 0);
-      for (int base = 8; base < A.ns; base += 8) sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+#ifndef BART_SUMS_TAIL4
+#define BART_SUMS_TAIL4 1
+#endif
+      for (int base = 8; base < A.ns; base += 8) {
+        if (BART_SUMS_TAIL4 && A.ns - base <= 4)  // a 4-slot tail (9-12 leaves: the common wide trees)
+          sums_pass<W, 4, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+        else
+          sums_pass<W, 8, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
+      }
   }
 }
 
@@ -461,7 +469,12 @@ __device__ __forceinline__ void refresh_count(uint32_t (&out)[W], const uint8_t 
   else if (ns <= 4)
     count_pass<W, 4>(out, G, slots, ns, 0, wrow, tid, lane);
   else
-    for (int base = 0; base < ns; base += 8) count_pass<W, 8>(out, G, slots, ns, base, wrow, tid, lane);
+    for (int base = 0; base < ns; base += 8) {
+      if (BART_SUMS_TAIL4 && ns - base <= 4)
+        count_pass<W, 4>(out, G, slots, ns, base, wrow, tid, lane);
+      else
+        count_pass<W, 8>(out, G, slots, ns, base, wrow, tid, lane);
+    }
 }
 
 // ------------------------------------------------------------ exchange
