@@ -1277,8 +1277,12 @@ __device__ __forceinline__ void stream_sums_all(const ChainDev &c, const Geom &G
     default:  // wide trees: further passes re-read the (updated) residuals
       // (per-width variants here cost 28% at n = 1e7: the stream loop spills)
       stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, 0, true);
-      for (int base = 8; base < A.ns; base += 8)
-        stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, base, false);
+      for (int base = 8; base < A.ns; base += 8) {
+        if (A.ns - base <= 4)  // a 4-slot tail (+9% at n = 1e7, where most trees have 9-12 slots)
+          stream_sums<4, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, base, false);
+        else
+          stream_sums<8, false>(c, G, A, lp32, lc32, dlt, S, tid, warp, lane, base, false);
+      }
   }
 }
 
@@ -1350,8 +1354,12 @@ __device__ __forceinline__ void stream_refresh_count_all(const ChainDev &c, cons
   else if (ns <= 4)
     stream_refresh_count<4>(c, G, j, hd, slots, wrow, tid, lane, 0, true);
   else
-    for (int base = 0; base < ns; base += 8)  // later groups re-read the refreshed row
-      stream_refresh_count<8>(c, G, j, hd, slots, wrow, tid, lane, base, base == 0);
+    for (int base = 0; base < ns; base += 8) {  // later groups re-read the refreshed row
+      if (ns - base <= 4)
+        stream_refresh_count<4>(c, G, j, hd, slots, wrow, tid, lane, base, base == 0);
+      else
+        stream_refresh_count<8>(c, G, j, hd, slots, wrow, tid, lane, base, base == 0);
+    }
 }
 
 __device__ __forceinline__ void stream_worker_loop(const ChainDev &c, SweepSmem &S, const Geom &G, int tid, int warp,
