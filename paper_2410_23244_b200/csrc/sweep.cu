@@ -374,6 +374,9 @@ __device__ __forceinline__ void sums_passes(float4 (&r)[W], const uint32_t (&lp)
 #ifndef BART_SUMS_TAIL4
 #define BART_SUMS_TAIL4 1
 #endif
+#ifndef BART_COUNT_TAIL4
+#define BART_COUNT_TAIL4 1
+#endif
       for (int base = 8; base < A.ns; base += 8) {
         if (BART_SUMS_TAIL4 && A.ns - base <= 4)  // a 4-slot tail (9-12 leaves: the common wide trees)
           sums_pass<W, 4, false, false>(r, lp, lc, A, G, dlt, S, tid, warp, lane, base);
@@ -470,7 +473,7 @@ __device__ __forceinline__ void refresh_count(uint32_t (&out)[W], const uint8_t 
     count_pass<W, 4>(out, G, slots, ns, 0, wrow, tid, lane);
   else
     for (int base = 0; base < ns; base += 8) {
-      if (BART_SUMS_TAIL4 && ns - base <= 4)
+      if (BART_COUNT_TAIL4 && ns - base <= 4)
         count_pass<W, 4>(out, G, slots, ns, base, wrow, tid, lane);
       else
         count_pass<W, 8>(out, G, slots, ns, base, wrow, tid, lane);

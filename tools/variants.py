@@ -35,6 +35,8 @@ def main():
             fk = d.get("forest_kernels") or {}
             fs = "  ".join(f"{k} {v['ms'] * 1e3:6.1f}us" for k, v in fk.items() if isinstance(v, dict))
             tr = (d.get("trees") or {}).get("mean_leaves")
+            fr = (d.get("fresh_chain") or {}).get("iters_per_s")
+            fs = f"fresh {fr:7.1f}  " + fs if fr else fs
             print(f"{name:24s} {d['value']:9.1f} {d['unit']}  e2e {d['e2e']['value']:8.1f}  ms {d['ms_per_step']:.4f}  "
                   f"leaves {tr}  {fs}", flush=True)
         except Exception:
